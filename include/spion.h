@@ -1,0 +1,200 @@
+/*
+ * spion.h — C ABI of libspion.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of SPION (arXiv 2309.12578): layer-wise sparsity
+ * pattern generation and block-sparse multi-head attention, forward and
+ * backward.
+ *
+ * Citations "P:N" are lines of the paper text; "Qk" are the
+ * readings of ambiguous passages listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points)
+ *  - Pointers named *_dev are DEVICE pointers; *_host are HOST pointers.
+ *    The caller owns every buffer, including workspaces; the library never
+ *    allocates device memory and keeps no state except a per-process cache
+ *    of driver entry points.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Every call is stream-ordered and asynchronous unless a *_host output
+ *    is requested, in which case the call synchronises `stream`.
+ *  - Errors never abort and never cross the ABI as exceptions: a call
+ *    returns SPION_OK or a status describing the first problem found on the
+ *    host (shape, parameter, alignment, workspace size, unsupported
+ *    configuration) before anything is launched, or SPION_ERR_CUDA if a
+ *    launch failed.  Data errors detectable only on the device (scores
+ *    outside [0,1] or NaN) set a flag word in the pattern workspace,
+ *    returned by spion_pattern_check().
+ *  - Layout of Q, K, V, O, dO, dQ, dK, dV: [bh][L][d], element (b, i, e) at
+ *    offset b*stride_bh + i*stride_l + e (elements, d contiguous), with
+ *    bh = batch * heads.  lse and D: [bh][L] fp32, contiguous.
+ *  - One block pattern per layer, shared by every (batch, head) (P:653,
+ *    reading Q16).
+ */
+#ifndef SPION_H
+#define SPION_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SPION_API __attribute__((visibility("default")))
+#else
+#define SPION_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPION_OK = 0,
+    SPION_ERR_SHAPE = 1,       /* L % block != 0, L <= 0, bad bh or d          */
+    SPION_ERR_PARAM = 2,       /* even filter, alpha outside (0,100), bad enum  */
+    SPION_ERR_DATA = 3,        /* scores outside [0,1] / NaN; non-binary mask   */
+    SPION_ERR_ALIGN = 4,       /* pointer or stride not 16-byte aligned          */
+    SPION_ERR_WORKSPACE = 5,   /* workspace / plan / capacity too small          */
+    SPION_ERR_CUDA = 6,        /* a CUDA runtime or driver call failed           */
+    SPION_ERR_UNSUPPORTED = 7  /* valid but not implemented (see each call)      */
+} spion_status;
+
+typedef enum { SPION_F32 = 0, SPION_BF16 = 1 } spion_dtype;
+
+/* Normaliser of the row softmax (Alg. 6; reading Q1).
+ * PAPER : Z = sum_stored exp(s-m) + (L - b_cnt) exp(-m)   (Alg. 6 l.15)
+ * MASKED: Z = sum_stored exp(s-m)                           (rows sum to 1) */
+typedef enum { SPION_SOFTMAX_PAPER = 0, SPION_SOFTMAX_MASKED = 1 } spion_softmax_mode;
+
+/* Threshold t of the flood fill (reading Q9).
+ * QUANTILE_LINEAR : t = alpha% quantile of pool_out, linear interpolation
+ *                   between order statistics (numpy/torch default), with
+ *                   hpos = ((double)(N-1) * alpha) / 100, N = nblk^2.
+ * QUANTILE_NEAREST: t = v[ceil(alpha/100 * N) - 1] (nearest rank).
+ * ABSOLUTE        : t given directly in pool-mean units (mean of the B x B
+ *                   block of conv_out with a diagonal filter of ones). */
+typedef enum {
+    SPION_TH_QUANTILE_LINEAR = 0,
+    SPION_TH_QUANTILE_NEAREST = 1,
+    SPION_TH_ABSOLUTE = 2
+} spion_threshold_kind;
+
+/* Block pattern in block-CSR + block-CSC form (CSR of P; the nearest
+ * neighbour upsampling of Alg. 3 l.11 is implicit: block
+ * (I,J) stands for the B x B all-ones square of P).  All pointers are
+ * device pointers owned by the caller.  Column (row) indices are strictly
+ * ascending within each row (column); brow_ptr[0] = 0, brow_ptr[nblk] =
+ * nnzb.  Generated patterns always contain the diagonal.
+ * `plan` holds the work lists the attention kernels consume (row tiles of
+ * the forward, column tiles of the backward); its contents are private. */
+typedef struct {
+    int32_t L, block, nblk, nnzb_cap; /* nblk = L / block; nnzb_cap >= nblk*nblk is always safe */
+    int32_t *brow_ptr;                /* [nblk+1] */
+    int32_t *bcol_idx;                /* [nnzb_cap] */
+    int32_t *bcol_ptr;                /* [nblk+1] */
+    int32_t *brow_idx;                /* [nnzb_cap] */
+    uint8_t *mask;                    /* [nblk*nblk] row-major fl_out, may be NULL */
+    int32_t *nnzb;                    /* [1] device scalar */
+    void *plan;                       /* >= spion_bsr_plan_bytes(L, block) bytes, 16-byte aligned */
+    size_t plan_bytes;
+} spion_bsr;
+
+/* Bytes of spion_bsr.plan for a pattern of this shape. */
+SPION_API size_t spion_bsr_plan_bytes(int32_t L, int32_t block);
+
+/* Bytes of device workspace spion_pattern needs (pool_out in int64 fixed
+ * point, the device flag word and selection scratch). */
+SPION_API size_t spion_pattern_workspace_bytes(int32_t L, int32_t block);
+
+/* Pattern generation, Alg. 3 with Alg. 4:
+ *   q = rint(A * 2^32) (reading Q8)  ->  Eq. 3 diagonal convolution, centred
+ *   window of `filter` taps, zero padding (reading Q5)  ->  Eq. 4
+ *   B x B pooling (sums, reading Q7)  ->  threshold t  ->
+ *   flood fill seeded at (0,i) and (j,0) (readings Q11-Q15, Q21)
+ *   ->  forced diagonal  ->  block-CSR/CSC and plan.
+ * scores_dev: [L][L] fp32 row-major, values in [0,1] (head-averaged A^s),
+ *   16-byte aligned; L % 4 == 0.
+ * block: B >= 1, L % B == 0; nblk = L/B must be <= 128 (else UNSUPPORTED).
+ * filter: F odd >= 1, with ceil(((F-1)/2)/B) <= 63.
+ * threshold: alpha in (0,100) for QUANTILE_*, t for ABSOLUTE.
+ * ws_dev: >= spion_pattern_workspace_bytes(L, block) bytes, 16-byte aligned.
+ * out: shape fields are filled in; pointer fields must be set by the caller
+ *   (nnzb_cap >= number of blocks produced, nblk*nblk is always enough).
+ * nnzb_host: if non-NULL, the call synchronises and stores nnzb there and
+ *   returns SPION_ERR_DATA if the device flagged bad scores.
+ * Results are bit-identical to the oracle (exact integer arithmetic). */
+SPION_API spion_status spion_pattern(const float *scores_dev, int32_t L, int32_t block, int32_t filter,
+                           double threshold, spion_threshold_kind kind, void *ws_dev, size_t ws_bytes,
+                           spion_bsr *out, int32_t *nnzb_host, void *stream);
+
+/* Synchronises `stream` and reads the device flag word of a pattern
+ * workspace: *flags_host = 0 if every score was finite and in [0,1]. */
+SPION_API spion_status spion_pattern_check(const void *ws_dev, int32_t *flags_host, void *stream);
+
+/* Block-CSR/CSC and plan from a caller-supplied block mask (e.g. SPION-C or
+ * a fixed pattern).  mask_dev: [nblk][nblk] uint8 in {0,1} (device); a
+ * non-binary byte sets *nnzb to -1 (and SPION_ERR_DATA if nnzb_host given).
+ * Empty rows are allowed (their outputs are zero, see spion_attn_fwd). */
+SPION_API spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t block, spion_bsr *out,
+                                 int32_t *nnzb_host, void *stream);
+
+/* Bytes of device workspace spion_attn_bwd needs: fp32 dQ accumulator
+ * [bh][L][d] and D_i = rowsum(dO*O) [bh][L].  spion_attn_fwd needs none. */
+SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt);
+
+/* Forward block-sparse attention, per (batch, head) b (Alg. 5 l.4-8,
+ * P:662-670; Eq. 5; Alg. 6):
+ *   s_ij = scale * Q_i . K_j for (floor(i/B), floor(j/B)) in the pattern (SDDMM)
+ *   p_ij = exp(s_ij - lse_i)                        (sparse softmax, mode)
+ *   O_i  = sum_stored p_ij V_j                      (SpMM)
+ *   lse_i = m_i + ln Z_i  (fp32; log-domain form of Alg. 6 l.15, reading Q2)
+ * Rows whose block-row is empty: O_i = 0, lse_i = ln L (PAPER) / -inf (MASKED).
+ * dt = SPION_BF16: bf16 Q/K/V/O, fp32 accumulation, P rounded to bf16 before
+ *   P.V on the tensor-core path (reading Q18).  Tensor-core (tcgen05) path
+ *   for block in {32, 64} and d == 64 with stride_l == d; other shapes run
+ *   the CUDA-core path.
+ * dt = SPION_F32: fp32 everywhere on CUDA cores (d <= 128, any block | L).
+ * scale: normally 1/sqrt(d) (Eq. 1; reading Q4).
+ * Pointers 16-byte aligned; strides in elements, multiples of 8 (bf16) or
+ * 4 (fp32).  d <= 128. */
+SPION_API spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, const void *V_dev, void *O_dev,
+                            float *lse_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
+                            int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,
+                            float scale, void *stream);
+
+/* Backward of spion_attn_fwd (the paper's custom autograd; formulas
+ * of reading Q17): with p_ij = exp(s_ij - lse_i) and D_i = dO_i . O_i,
+ *   dp_ij = dO_i . V_j ; ds_ij = p_ij (dp_ij - D_i)
+ *   dQ_i = scale sum_j ds_ij K_j ; dK_j = scale sum_i ds_ij Q_i ; dV_j = sum_i p_ij dO_i
+ * The same formulas hold in both modes (the implicit zeros act only
+ * through Z).  O and lse are the outputs of spion_attn_fwd.  dQ, dK, dV use
+ * the same layout and strides as Q.  ws_dev: >= spion_attn_workspace_bytes. */
+SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
+                            const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev,
+                            void *dV_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
+                            int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,
+                            float scale, void *ws_dev, size_t ws_bytes, void *stream);
+
+/* One whole step of the hot path from HOST buffers (the end-to-end call):
+ * copies scores, Q, K, V, dO host->device, runs spion_pattern,
+ * spion_attn_fwd and spion_attn_bwd, and copies O, lse, dQ, dK, dV back.
+ * Tensors are contiguous [bh][L][d] (stride_l = d).  Host buffers should be
+ * pinned for asynchronous copies.  dev_arena: caller-owned device memory of
+ * >= spion_step_arena_bytes(...) bytes.  Synchronises `stream` and returns
+ * nnzb in *nnzb_host (may be NULL). */
+SPION_API size_t spion_step_arena_bytes(int64_t bh, int32_t L, int32_t d, int32_t block, spion_dtype dt);
+SPION_API spion_status spion_step_host(const float *scores_host, const void *Q_host, const void *K_host,
+                             const void *V_host, const void *dO_host, void *O_host, float *lse_host,
+                             void *dQ_host, void *dK_host, void *dV_host, int64_t bh, int32_t L, int32_t d,
+                             int32_t block, int32_t filter, double threshold, spion_threshold_kind kind,
+                             spion_dtype dt, spion_softmax_mode mode, float scale, void *dev_arena,
+                             size_t arena_bytes, int32_t *nnzb_host, void *stream);
+
+/* Number of this library's kernels launched by this thread since process
+ * start (host-side counter, for the bench's gpu_launches claim). */
+SPION_API int64_t spion_launch_count(void);
+
+/* Human-readable status. */
+SPION_API const char *spion_status_str(spion_status s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPION_H */

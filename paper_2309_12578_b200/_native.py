@@ -1,0 +1,82 @@
+"""ctypes declarations of libspion.so (include/spion.h).  Marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(PKG, "lib", "libspion.so")
+
+OK = 0
+STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace", 6: "cuda", 7: "unsupported"}
+F32, BF16 = 0, 1
+SOFTMAX = {"paper": 0, "masked": 1}
+THRESH = {"linear": 0, "nearest": 1, "absolute": 2}
+
+
+class SpionError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {STATUS.get(status, status)} ({status})")
+
+
+class BSR(ctypes.Structure):
+    _fields_ = [
+        ("L", ctypes.c_int32), ("block", ctypes.c_int32), ("nblk", ctypes.c_int32), ("nnzb_cap", ctypes.c_int32),
+        ("brow_ptr", ctypes.c_void_p), ("bcol_idx", ctypes.c_void_p), ("bcol_ptr", ctypes.c_void_p),
+        ("brow_idx", ctypes.c_void_p), ("mask", ctypes.c_void_p), ("nnzb", ctypes.c_void_p),
+        ("plan", ctypes.c_void_p), ("plan_bytes", ctypes.c_size_t),
+    ]
+
+
+EXPORTS = {
+    "spion_bsr_plan_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "spion_pattern_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "spion_pattern": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(BSR),
+                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_pattern_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_bsr_from_mask": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BSR),
+                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_attn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int]),
+    "spion_attn_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_int, ctypes.POINTER(BSR), ctypes.c_int, ctypes.c_float,
+                                      ctypes.c_void_p]),
+    "spion_attn_bwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_int, ctypes.POINTER(BSR), ctypes.c_int, ctypes.c_float,
+                                      ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "spion_step_arena_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_int]),
+    "spion_step_host": (ctypes.c_int, [ctypes.c_void_p] * 10 + [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                                                ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                                                ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                                ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t,
+                                                                ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_launch_count": (ctypes.c_int64, []),
+    "spion_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libspion.so (fails loudly if the extension has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError(f"libspion.so not found at {SO_PATH}; run __graft_entry__.build()")
+        L = ctypes.CDLL(SO_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str):
+    if status != OK:
+        raise SpionError(status, what)

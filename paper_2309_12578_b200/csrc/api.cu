@@ -1,0 +1,351 @@
+// api.cu — the C ABI of libspion.so (include/spion.h): validation, dispatch,
+// workspace carving and the host-buffer step.  No arithmetic of the method
+// lives here except the host-side threshold rank (Alg. 3 / P:600), which is a
+// scalar computed once per call.
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "attn.cuh"
+
+namespace spion {
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void report_cuda_error(cudaError_t e, const char *what, const char *file, int line) {
+    static const bool on = getenv("SPION_DEBUG") != nullptr;
+    if (on) fprintf(stderr, "[spion] %s:%d %s -> %s\n", file, line, what, cudaGetErrorString(e));
+}
+}  // namespace spion
+
+using namespace spion;
+
+extern "C" {
+
+int64_t spion_launch_count(void) { return (int64_t)g_launches.load(); }
+
+const char *spion_status_str(spion_status s) {
+    switch (s) {
+        case SPION_OK: return "ok";
+        case SPION_ERR_SHAPE: return "shape error (L % block, L, bh or d)";
+        case SPION_ERR_PARAM: return "parameter error (filter, threshold, enum)";
+        case SPION_ERR_DATA: return "data error (scores outside [0,1]/NaN or non-binary mask)";
+        case SPION_ERR_ALIGN: return "alignment error (pointers/strides must be 16-byte aligned)";
+        case SPION_ERR_WORKSPACE: return "workspace, plan or capacity too small";
+        case SPION_ERR_CUDA: return "CUDA error";
+        case SPION_ERR_UNSUPPORTED: return "unsupported configuration";
+    }
+    return "unknown status";
+}
+
+size_t spion_bsr_plan_bytes(int32_t L, int32_t block) {
+    if (L <= 0 || block <= 0 || L % block) return 0;
+    PlanLayout pl(L / block, block);
+    return round_up(pl.words * 4, 256);
+}
+
+size_t spion_pattern_workspace_bytes(int32_t L, int32_t block) {
+    if (L <= 0 || block <= 0 || L % block) return 0;
+    return pattern_ws_bytes(L, block);
+}
+
+static spion_status check_bsr_out(const spion_bsr *out, int32_t L, int32_t block) {
+    if (!out || !out->brow_ptr || !out->bcol_idx || !out->bcol_ptr || !out->brow_idx || !out->nnzb)
+        return SPION_ERR_PARAM;
+    if (out->plan && out->plan_bytes < spion_bsr_plan_bytes(L, block)) return SPION_ERR_WORKSPACE;
+    if (out->plan && !aligned16(out->plan)) return SPION_ERR_ALIGN;
+    if (out->nnzb_cap < L / block) return SPION_ERR_WORKSPACE;  // the diagonal alone needs nblk
+    return SPION_OK;
+}
+
+spion_status spion_pattern(const float *scores_dev, int32_t L, int32_t block, int32_t filter, double threshold,
+                           spion_threshold_kind kind, void *ws_dev, size_t ws_bytes, spion_bsr *out,
+                           int32_t *nnzb_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (L <= 0 || block <= 0 || L % block) return SPION_ERR_SHAPE;
+    if (filter < 1 || filter % 2 == 0) return SPION_ERR_PARAM;
+    if (!scores_dev || !ws_dev) return SPION_ERR_PARAM;
+    if (!aligned16(scores_dev) || !aligned16(ws_dev) || L % 4) return SPION_ERR_ALIGN;
+    const int n = L / block;
+    if (n > 128) return SPION_ERR_UNSUPPORTED;
+    const int h = (filter - 1) / 2;
+    if ((h + block - 1) / block > 63) return SPION_ERR_UNSUPPORTED;
+    if (ws_bytes < pattern_ws_bytes(L, block)) return SPION_ERR_WORKSPACE;
+    spion_status st = check_bsr_out(out, L, block);
+    if (st) return st;
+    out->L = L;
+    out->block = block;
+    out->nblk = n;
+    const long long N = (long long)n * n;
+    long long lo = 0, T_abs = 0;
+    int frac_pos = 0;
+    switch (kind) {
+        case SPION_TH_QUANTILE_LINEAR: {
+            if (!(threshold > 0.0 && threshold < 100.0)) return SPION_ERR_PARAM;
+            const double hpos = ((double)(N - 1) * threshold) / 100.0;
+            lo = (long long)floor(hpos);
+            const double frac = hpos - (double)lo;
+            if (lo >= N - 1) { lo = N - 1; frac_pos = 0; }
+            else frac_pos = frac > 0.0;
+            break;
+        }
+        case SPION_TH_QUANTILE_NEAREST: {
+            if (!(threshold > 0.0 && threshold < 100.0)) return SPION_ERR_PARAM;
+            long long k = (long long)ceil(threshold / 100.0 * (double)N) - 1;
+            if (k < 0) k = 0;
+            if (k > N - 1) k = N - 1;
+            lo = k;
+            break;
+        }
+        case SPION_TH_ABSOLUTE: {
+            if (!isfinite(threshold)) return SPION_ERR_PARAM;
+            // gt(x) <=> x > t * B^2 * 2^32 (pool-mean units); x integral => x > floor(thr)
+            const double thr = threshold * (double)((long long)block * block) * 4294967296.0;
+            if (thr < 0.0) T_abs = -1;
+            else if (thr >= 9.2e18) T_abs = 0x7fffffffffffffffLL;
+            else T_abs = (long long)floor(thr);
+            break;
+        }
+        default: return SPION_ERR_PARAM;
+    }
+    st = launch_pattern(scores_dev, L, block, filter, (int)kind, lo, frac_pos, T_abs, ws_dev, out, s);
+    if (st) return st;
+    if (nnzb_host) {
+        int flags = 0;
+        SPION_CUDA_TRY(cudaMemcpyAsync(nnzb_host, out->nnzb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SPION_CUDA_TRY(cudaMemcpyAsync(&flags, ws_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SPION_CUDA_TRY(cudaStreamSynchronize(s));
+        if (flags & FLAG_BAD_SCORE) return SPION_ERR_DATA;
+        if (flags & FLAG_CAPACITY) return SPION_ERR_WORKSPACE;
+    }
+    return SPION_OK;
+}
+
+spion_status spion_pattern_check(const void *ws_dev, int32_t *flags_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ws_dev || !flags_host) return SPION_ERR_PARAM;
+    SPION_CUDA_TRY(cudaMemcpyAsync(flags_host, ws_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPION_CUDA_TRY(cudaStreamSynchronize(s));
+    return SPION_OK;
+}
+
+spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t block, spion_bsr *out,
+                                 int32_t *nnzb_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (L <= 0 || block <= 0 || L % block) return SPION_ERR_SHAPE;
+    if (!mask_dev) return SPION_ERR_PARAM;
+    const int n = L / block;
+    if (n > 128) return SPION_ERR_UNSUPPORTED;
+    if (out && out->nnzb_cap < 0) return SPION_ERR_WORKSPACE;
+    if (!out || !out->brow_ptr || !out->bcol_idx || !out->bcol_ptr || !out->brow_idx || !out->nnzb)
+        return SPION_ERR_PARAM;
+    if (out->plan && (out->plan_bytes < spion_bsr_plan_bytes(L, block) || !aligned16(out->plan)))
+        return SPION_ERR_WORKSPACE;
+    out->L = L;
+    out->block = block;
+    out->nblk = n;
+    spion_status st = launch_bsr_from_mask(mask_dev, L, block, out, nullptr, s);
+    if (st) return st;
+    if (nnzb_host) {
+        SPION_CUDA_TRY(cudaMemcpyAsync(nnzb_host, out->nnzb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SPION_CUDA_TRY(cudaStreamSynchronize(s));
+        if (*nnzb_host < 0) return SPION_ERR_DATA;
+        if (*nnzb_host > out->nnzb_cap) return SPION_ERR_WORKSPACE;
+    }
+    return SPION_OK;
+}
+
+size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt) {
+    (void)dt;
+    if (bh <= 0 || L <= 0 || d <= 0) return 0;
+    return round_up((size_t)bh * L * d * 4, 256) + round_up((size_t)bh * L * 4, 256);
+}
+
+static spion_status check_attn_common(const void *Q, const void *K, const void *V, int64_t bh, int32_t L,
+                                      int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
+                                      const spion_bsr *pat, int mode) {
+    if (!Q || !K || !V || !pat) return SPION_ERR_PARAM;
+    if (bh <= 0 || L <= 0 || d <= 0 || d > 128) return SPION_ERR_SHAPE;
+    if (pat->L != L || pat->block <= 0 || L % pat->block || pat->nblk != L / pat->block) return SPION_ERR_SHAPE;
+    if (dt != SPION_F32 && dt != SPION_BF16) return SPION_ERR_PARAM;
+    if (mode != SPION_SOFTMAX_PAPER && mode != SPION_SOFTMAX_MASKED) return SPION_ERR_PARAM;
+    if (stride_l < d || stride_bh < d) return SPION_ERR_SHAPE;
+    const int vec = dt == SPION_BF16 ? 8 : 4;
+    if (stride_l % vec || stride_bh % vec) return SPION_ERR_ALIGN;
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(V)) return SPION_ERR_ALIGN;
+    if (!pat->brow_ptr || !pat->bcol_idx || !pat->bcol_ptr || !pat->brow_idx) return SPION_ERR_PARAM;
+    return SPION_OK;
+}
+
+static AttnArgs make_args(const void *Q, const void *K, const void *V, int64_t bh, int32_t L, int32_t d,
+                          int64_t stride_bh, int64_t stride_l, const spion_bsr *pat, int mode, float scale) {
+    AttnArgs a;
+    memset(&a, 0, sizeof(a));
+    a.Q = Q;
+    a.K = K;
+    a.V = V;
+    a.bh = bh;
+    a.L = L;
+    a.d = d;
+    a.stride_bh = stride_bh;
+    a.stride_l = stride_l;
+    a.B = pat->block;
+    a.n = pat->nblk;
+    a.mode = mode;
+    a.scale = scale;
+    a.brow_ptr = pat->brow_ptr;
+    a.bcol_idx = pat->bcol_idx;
+    a.bcol_ptr = pat->bcol_ptr;
+    a.brow_idx = pat->brow_idx;
+    a.plan = static_cast<const int *>(pat->plan);
+    return a;
+}
+
+spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, const void *V_dev, void *O_dev, float *lse_dev,
+                            int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
+                            const spion_bsr *pat, spion_softmax_mode mode, float scale, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    spion_status st = check_attn_common(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, dt, pat, mode);
+    if (st) return st;
+    if (!O_dev || !lse_dev) return SPION_ERR_PARAM;
+    if (!aligned16(O_dev) || !aligned16(lse_dev)) return SPION_ERR_ALIGN;
+    if (bh > 65535) return SPION_ERR_UNSUPPORTED;
+    AttnArgs a = make_args(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, pat, mode, scale);
+    a.Oout = O_dev;
+    a.lse_out = lse_dev;
+    if (dt == SPION_BF16 && tc_supported(a, dt)) return launch_fwd_tc(a, s);
+    if (!simt_supported(a.B, d)) return SPION_ERR_UNSUPPORTED;
+    return launch_fwd_simt(a, dt, s);
+}
+
+spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
+                            const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev, void *dV_dev,
+                            int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
+                            const spion_bsr *pat, spion_softmax_mode mode, float scale, void *ws_dev,
+                            size_t ws_bytes, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    spion_status st = check_attn_common(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, dt, pat, mode);
+    if (st) return st;
+    if (!O_dev || !dO_dev || !lse_dev || !dQ_dev || !dK_dev || !dV_dev || !ws_dev) return SPION_ERR_PARAM;
+    if (!aligned16(O_dev) || !aligned16(dO_dev) || !aligned16(dQ_dev) || !aligned16(dK_dev) ||
+        !aligned16(dV_dev) || !aligned16(ws_dev) || !aligned16(lse_dev))
+        return SPION_ERR_ALIGN;
+    if (ws_bytes < spion_attn_workspace_bytes(bh, L, d, dt)) return SPION_ERR_WORKSPACE;
+    if (bh > 65535) return SPION_ERR_UNSUPPORTED;
+    AttnArgs a = make_args(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, pat, mode, scale);
+    a.O = O_dev;
+    a.dO = dO_dev;
+    a.lse = lse_dev;
+    a.dQ = dQ_dev;
+    a.dK = dK_dev;
+    a.dV = dV_dev;
+    a.dQacc = static_cast<float *>(ws_dev);
+    float *D = reinterpret_cast<float *>(static_cast<char *>(ws_dev) + round_up((size_t)bh * L * d * 4, 256));
+    a.D = D;
+    if (dt == SPION_BF16 && tc_supported(a, dt)) return launch_bwd_tc(a, s);
+    if (!simt_supported(a.B, d)) return SPION_ERR_UNSUPPORTED;
+    st = launch_bwd_preprocess(a, dt, D, s);
+    if (st) return st;
+    return launch_bwd_simt(a, dt, s);
+}
+
+// ------------------------------------------------------------------ host-buffer step
+struct Arena {
+    size_t scores, Q, K, V, dO, O, lse, dQ, dK, dV, pws, aws, brow_ptr, bcol_idx, bcol_ptr, brow_idx, mask, nnzb,
+        plan, total;
+};
+
+static Arena arena_layout(int64_t bh, int32_t L, int32_t d, int32_t block, spion_dtype dt) {
+    Arena A;
+    const size_t elt = dt == SPION_BF16 ? 2 : 4;
+    const size_t t = (size_t)bh * L * d * elt;
+    const int n = L / block;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += round_up(bytes, 256); return r; };
+    A.scores = take((size_t)L * L * 4);
+    A.Q = take(t);
+    A.K = take(t);
+    A.V = take(t);
+    A.dO = take(t);
+    A.O = take(t);
+    A.lse = take((size_t)bh * L * 4);
+    A.dQ = take(t);
+    A.dK = take(t);
+    A.dV = take(t);
+    A.pws = take(pattern_ws_bytes(L, block));
+    A.aws = take(spion_attn_workspace_bytes(bh, L, d, dt));
+    A.brow_ptr = take((size_t)(n + 1) * 4);
+    A.bcol_idx = take((size_t)n * n * 4);
+    A.bcol_ptr = take((size_t)(n + 1) * 4);
+    A.brow_idx = take((size_t)n * n * 4);
+    A.mask = take((size_t)n * n);
+    A.nnzb = take(16);
+    A.plan = take(spion_bsr_plan_bytes(L, block));
+    A.total = o;
+    return A;
+}
+
+size_t spion_step_arena_bytes(int64_t bh, int32_t L, int32_t d, int32_t block, spion_dtype dt) {
+    if (bh <= 0 || L <= 0 || d <= 0 || block <= 0 || L % block) return 0;
+    return arena_layout(bh, L, d, block, dt).total;
+}
+
+spion_status spion_step_host(const float *scores_host, const void *Q_host, const void *K_host, const void *V_host,
+                             const void *dO_host, void *O_host, float *lse_host, void *dQ_host, void *dK_host,
+                             void *dV_host, int64_t bh, int32_t L, int32_t d, int32_t block, int32_t filter,
+                             double threshold, spion_threshold_kind kind, spion_dtype dt, spion_softmax_mode mode,
+                             float scale, void *dev_arena, size_t arena_bytes, int32_t *nnzb_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (bh <= 0 || L <= 0 || d <= 0 || block <= 0 || L % block) return SPION_ERR_SHAPE;
+    if (!dev_arena || !aligned16(dev_arena)) return SPION_ERR_ALIGN;
+    Arena A = arena_layout(bh, L, d, block, dt);
+    if (arena_bytes < A.total) return SPION_ERR_WORKSPACE;
+    char *base = static_cast<char *>(dev_arena);
+    const size_t elt = dt == SPION_BF16 ? 2 : 4;
+    const size_t t = (size_t)bh * L * d * elt;
+    const int n = L / block;
+    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.scores, scores_host, (size_t)L * L * 4, cudaMemcpyHostToDevice, s));
+    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.Q, Q_host, t, cudaMemcpyHostToDevice, s));
+    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.K, K_host, t, cudaMemcpyHostToDevice, s));
+    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.V, V_host, t, cudaMemcpyHostToDevice, s));
+    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.dO, dO_host, t, cudaMemcpyHostToDevice, s));
+    spion_bsr bsr;
+    memset(&bsr, 0, sizeof(bsr));
+    bsr.nnzb_cap = n * n;
+    bsr.brow_ptr = reinterpret_cast<int32_t *>(base + A.brow_ptr);
+    bsr.bcol_idx = reinterpret_cast<int32_t *>(base + A.bcol_idx);
+    bsr.bcol_ptr = reinterpret_cast<int32_t *>(base + A.bcol_ptr);
+    bsr.brow_idx = reinterpret_cast<int32_t *>(base + A.brow_idx);
+    bsr.mask = reinterpret_cast<uint8_t *>(base + A.mask);
+    bsr.nnzb = reinterpret_cast<int32_t *>(base + A.nnzb);
+    bsr.plan = base + A.plan;
+    bsr.plan_bytes = spion_bsr_plan_bytes(L, block);
+    spion_status st = spion_pattern(reinterpret_cast<const float *>(base + A.scores), L, block, filter, threshold,
+                                    kind, base + A.pws, pattern_ws_bytes(L, block), &bsr, nullptr, stream);
+    if (st) return st;
+    st = spion_attn_fwd(base + A.Q, base + A.K, base + A.V, base + A.O, reinterpret_cast<float *>(base + A.lse), bh,
+                        L, d, (int64_t)L * d, d, dt, &bsr, mode, scale, stream);
+    if (st) return st;
+    st = spion_attn_bwd(base + A.Q, base + A.K, base + A.V, base + A.O, base + A.dO,
+                        reinterpret_cast<const float *>(base + A.lse), base + A.dQ, base + A.dK, base + A.dV, bh, L,
+                        d, (int64_t)L * d, d, dt, &bsr, mode, scale, base + A.aws,
+                        spion_attn_workspace_bytes(bh, L, d, dt), stream);
+    if (st) return st;
+    if (O_host) SPION_CUDA_TRY(cudaMemcpyAsync(O_host, base + A.O, t, cudaMemcpyDeviceToHost, s));
+    if (lse_host) SPION_CUDA_TRY(cudaMemcpyAsync(lse_host, base + A.lse, (size_t)bh * L * 4, cudaMemcpyDeviceToHost, s));
+    if (dQ_host) SPION_CUDA_TRY(cudaMemcpyAsync(dQ_host, base + A.dQ, t, cudaMemcpyDeviceToHost, s));
+    if (dK_host) SPION_CUDA_TRY(cudaMemcpyAsync(dK_host, base + A.dK, t, cudaMemcpyDeviceToHost, s));
+    if (dV_host) SPION_CUDA_TRY(cudaMemcpyAsync(dV_host, base + A.dV, t, cudaMemcpyDeviceToHost, s));
+    int32_t nnzb = 0;
+    SPION_CUDA_TRY(cudaMemcpyAsync(&nnzb, bsr.nnzb, 4, cudaMemcpyDeviceToHost, s));
+    int flags = 0;
+    SPION_CUDA_TRY(cudaMemcpyAsync(&flags, base + A.pws, 4, cudaMemcpyDeviceToHost, s));
+    SPION_CUDA_TRY(cudaStreamSynchronize(s));
+    if (nnzb_host) *nnzb_host = nnzb;
+    if (flags & FLAG_BAD_SCORE) return SPION_ERR_DATA;
+    return SPION_OK;
+}
+
+}  // extern "C"

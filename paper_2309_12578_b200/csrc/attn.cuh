@@ -1,0 +1,37 @@
+// attn.cuh — internal interface between the ABI layer and the attention kernels.
+#pragma once
+#include "common.cuh"
+
+namespace spion {
+
+struct AttnArgs {
+    const void *Q, *K, *V, *O, *dO;
+    void *Oout, *dQ, *dK, *dV;
+    float *lse_out;
+    const float *lse, *D;
+    float *dQacc;  // fp32 [bh][L][d] workspace (tensor-core backward)
+    int64_t bh, stride_bh, stride_l;
+    int L, d, B, n;
+    int mode;
+    float scale;
+    const int *brow_ptr, *bcol_idx, *bcol_ptr, *brow_idx;
+    const int *plan;
+};
+
+bool simt_supported(int B, int d);
+spion_status launch_fwd_simt(const AttnArgs &a, spion_dtype dt, cudaStream_t s);
+spion_status launch_bwd_preprocess(const AttnArgs &a, spion_dtype dt, float *D, cudaStream_t s);
+spion_status launch_bwd_simt(const AttnArgs &a, spion_dtype dt, cudaStream_t s);
+
+// tensor-core (tcgen05) path; attn_tc.cu
+bool tc_supported(const AttnArgs &a, spion_dtype dt);
+spion_status launch_fwd_tc(const AttnArgs &a, cudaStream_t s);
+spion_status launch_bwd_tc(const AttnArgs &a, cudaStream_t s);
+
+// pattern kernels; pattern.cu
+size_t pattern_ws_bytes(int L, int block);
+spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos,
+                            long long T_abs, void *ws, spion_bsr *out, cudaStream_t s);
+spion_status launch_bsr_from_mask(const uint8_t *mask, int L, int B, spion_bsr *out, int *flags, cudaStream_t s);
+
+}  // namespace spion

@@ -1,0 +1,226 @@
+"""PyTorch-facing API of the SPION hot path (argument marshalling only).
+
+Every step of the computation runs in libspion.so's CUDA kernels; this module
+owns device memory (torch tensors), picks the current CUDA stream and passes
+plain pointers through the C ABI (include/spion.h).  There is no CPU or
+PyTorch fallback: a missing library or a non-CUDA tensor raises.
+
+    bsr = pattern(scores, block=64, filter=31, alpha=99.0)     # Alg. 3/4
+    o, lse = attn_fwd(q, k, v, bsr)                            # Alg. 5/6, Eq. 5
+    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, bsr)            # custom autograd
+    o = attention(q, k, v, bsr)                                # autograd.Function
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _native as N
+
+
+def _stream(dev: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _p(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError("spion kernels need CUDA tensors (there is no CPU path)")
+
+
+@dataclass
+class BlockPattern:
+    """Block-CSR + block-CSC of a layer's pattern, and the kernels' work plan (device tensors)."""
+    L: int
+    block: int
+    nblk: int
+    brow_ptr: torch.Tensor
+    bcol_idx: torch.Tensor
+    bcol_ptr: torch.Tensor
+    brow_idx: torch.Tensor
+    mask: torch.Tensor
+    nnzb_dev: torch.Tensor
+    plan: torch.Tensor
+    workspace: Optional[torch.Tensor] = None
+    flat: Optional[torch.Tensor] = None
+
+    def c_struct(self) -> N.BSR:
+        s = N.BSR()
+        s.L, s.block, s.nblk = self.L, self.block, self.nblk
+        s.nnzb_cap = self.bcol_idx.numel()
+        s.brow_ptr, s.bcol_idx = self.brow_ptr.data_ptr(), self.bcol_idx.data_ptr()
+        s.bcol_ptr, s.brow_idx = self.bcol_ptr.data_ptr(), self.brow_idx.data_ptr()
+        s.mask, s.nnzb = self.mask.data_ptr(), self.nnzb_dev.data_ptr()
+        s.plan, s.plan_bytes = self.plan.data_ptr(), self.plan.numel()
+        return s
+
+    @property
+    def nnzb(self) -> int:
+        return int(self.nnzb_dev[0].item())
+
+    def csr(self):
+        k = self.nnzb
+        return self.brow_ptr, self.bcol_idx[:k]
+
+    def csc(self):
+        k = self.nnzb
+        return self.bcol_ptr, self.brow_idx[:k]
+
+
+def empty_pattern(L: int, block: int, device) -> BlockPattern:
+    """Allocate a pattern as views into ONE int32 buffer (``.flat``), so a rank can
+    broadcast a whole pattern with a single collective."""
+    lib = N.lib()
+    n = L // block
+    plan_bytes = lib.spion_bsr_plan_bytes(L, block)
+    sizes = [n + 1, n * n, n + 1, n * n, (n * n + 3) // 4, 4, (plan_bytes + 3) // 4]
+    offs = [0]
+    for sz in sizes:
+        offs.append(offs[-1] + ((sz + 3) // 4) * 4)  # 16-byte aligned views
+    flat = torch.zeros(offs[-1], dtype=torch.int32, device=device)
+    v = [flat[offs[i]:offs[i] + sizes[i]] for i in range(len(sizes))]
+    bp = BlockPattern(
+        L=L, block=block, nblk=n, brow_ptr=v[0], bcol_idx=v[1], bcol_ptr=v[2], brow_idx=v[3],
+        mask=v[4].view(torch.uint8)[: n * n], nnzb_dev=v[5], plan=v[6].view(torch.uint8)[:plan_bytes],
+    )
+    bp.flat = flat
+    return bp
+
+
+def pattern(scores: torch.Tensor, block: int, filter: int = 31, alpha: Optional[float] = None,
+            t: Optional[float] = None, kind: str = "linear", out: Optional[BlockPattern] = None,
+            sync: bool = False) -> BlockPattern:
+    """Alg. 3: scores [L][L] fp32 in [0,1] -> block pattern.
+
+    Give ``alpha`` (percent, quantile threshold, ``kind`` linear|nearest) or ``t``
+    (absolute threshold in pool-mean units)."""
+    _require_cuda(scores)
+    if scores.dtype != torch.float32 or scores.dim() != 2 or scores.shape[0] != scores.shape[1]:
+        raise ValueError("scores must be a square fp32 matrix")
+    scores = scores.contiguous()
+    L = scores.shape[0]
+    lib = N.lib()
+    if t is not None:
+        kind, theta = "absolute", float(t)
+    else:
+        if alpha is None:
+            raise ValueError("give alpha or t")
+        theta = float(alpha)
+    bp = out if out is not None else empty_pattern(L, block, scores.device)
+    ws_bytes = lib.spion_pattern_workspace_bytes(L, block)
+    if bp.workspace is None or bp.workspace.numel() < ws_bytes:
+        bp.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=scores.device)
+    s = bp.c_struct()
+    nnz = ctypes.c_int32(0)
+    st = lib.spion_pattern(_p(scores), L, block, filter, theta, N.THRESH[kind], _p(bp.workspace), ws_bytes,
+                           ctypes.byref(s), ctypes.byref(nnz) if sync else None, _stream(scores.device))
+    N.check(st, "spion_pattern")
+    return bp
+
+
+def bsr_from_mask(mask: torch.Tensor, L: int, block: int, out: Optional[BlockPattern] = None) -> BlockPattern:
+    """Block pattern from a caller-supplied [nblk][nblk] {0,1} uint8 mask (device)."""
+    _require_cuda(mask)
+    mask = mask.to(torch.uint8).contiguous()
+    bp = out if out is not None else empty_pattern(L, block, mask.device)
+    s = bp.c_struct()
+    nnz = ctypes.c_int32(0)
+    st = N.lib().spion_bsr_from_mask(_p(mask), L, block, ctypes.byref(s), ctypes.byref(nnz), _stream(mask.device))
+    N.check(st, "spion_bsr_from_mask")
+    return bp
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return N.BF16
+    if t.dtype == torch.float32:
+        return N.F32
+    raise ValueError("Q/K/V must be bf16 or fp32")
+
+
+def _layout(q: torch.Tensor):
+    if q.dim() != 3 or q.stride(2) != 1:
+        raise ValueError("expected [bh][L][d] with d contiguous")
+    return q.shape[0], q.shape[1], q.shape[2], q.stride(0), q.stride(1)
+
+
+def attn_fwd(q, k, v, bp: BlockPattern, mode: str = "paper", scale: Optional[float] = None,
+             out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None):
+    """O, lse of block-sparse attention (Eq. 5 / Alg. 6).  q,k,v: [bh][L][d], same strides."""
+    _require_cuda(q, k, v)
+    bh, L, d, sb, sl = _layout(q)
+    if k.stride() != q.stride() or v.stride() != q.stride() or k.shape != q.shape or v.shape != q.shape:
+        raise ValueError("q, k, v must share shape and strides")
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if out is None:
+        out = torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device)
+    if lse is None:
+        lse = torch.empty((bh, L), dtype=torch.float32, device=q.device)
+    s = bp.c_struct()
+    st = N.lib().spion_attn_fwd(_p(q), _p(k), _p(v), _p(out), _p(lse), bh, L, d, sb, sl, _dtype_code(q),
+                                ctypes.byref(s), N.SOFTMAX[mode], float(scale), _stream(q.device))
+    N.check(st, "spion_attn_fwd")
+    return out, lse
+
+
+def attn_workspace(bh: int, L: int, d: int, dtype, device) -> torch.Tensor:
+    nb = N.lib().spion_attn_workspace_bytes(bh, L, d, N.BF16 if dtype == torch.bfloat16 else N.F32)
+    return torch.empty(nb, dtype=torch.uint8, device=device)
+
+
+def attn_bwd(q, k, v, o, do, lse, bp: BlockPattern, mode: str = "paper", scale: Optional[float] = None,
+             workspace: Optional[torch.Tensor] = None, dq=None, dk=None, dv=None):
+    """dQ, dK, dV of block-sparse attention (reading Q17)."""
+    _require_cuda(q, k, v, o, do, lse)
+    bh, L, d, sb, sl = _layout(q)
+    for t in (k, v, o, do):
+        if t.stride() != q.stride() or t.shape != q.shape:
+            raise ValueError("q, k, v, o, do must share shape and strides")
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if workspace is None:
+        workspace = attn_workspace(bh, L, d, q.dtype, q.device)
+    mk = lambda: torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device)
+    dq = mk() if dq is None else dq
+    dk = mk() if dk is None else dk
+    dv = mk() if dv is None else dv
+    s = bp.c_struct()
+    st = N.lib().spion_attn_bwd(_p(q), _p(k), _p(v), _p(o), _p(do), _p(lse), _p(dq), _p(dk), _p(dv), bh, L, d, sb,
+                                sl, _dtype_code(q), ctypes.byref(s), N.SOFTMAX[mode], float(scale), _p(workspace),
+                                workspace.numel(), _stream(q.device))
+    N.check(st, "spion_attn_bwd")
+    return dq, dk, dv
+
+
+class _SparseAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, bp, mode, scale):
+        o, lse = attn_fwd(q, k, v, bp, mode, scale)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.bp, ctx.mode, ctx.scale = bp, mode, scale
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        do = do.contiguous() if do.stride() != q.stride() else do
+        dq, dk, dv = attn_bwd(q, k, v, o, do, lse, ctx.bp, ctx.mode, ctx.scale)
+        return dq, dk, dv, None, None, None
+
+
+def attention(q, k, v, bp: BlockPattern, mode: str = "paper", scale: Optional[float] = None):
+    """Differentiable block-sparse attention (the paper's sparseMHA core, Alg. 5 l.4-8)."""
+    return _SparseAttention.apply(q, k, v, bp, mode, scale)
+
+
+def launch_count() -> int:
+    return int(N.lib().spion_launch_count())

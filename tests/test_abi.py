@@ -1,0 +1,103 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports every
+symbol include/spion.h declares, and rejects bad arguments before launching anything."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2309_12578_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "spion.h")).read()
+    return sorted(set(re.findall(r"SPION_API\s+[\w\s\*]+?\b(spion_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    names = _declared()
+    assert len(names) >= 12
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(N.EXPORTS), "ctypes table out of sync with include/spion.h"
+
+
+def test_no_oracle_in_product_package():
+    pkg = os.path.join(ROOT, "paper_2309_12578_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "spion_oracle" not in txt, f
+
+
+def test_sizes():
+    lib = N.lib()
+    assert lib.spion_bsr_plan_bytes(4096, 64) > 0
+    assert lib.spion_bsr_plan_bytes(100, 64) == 0
+    assert lib.spion_pattern_workspace_bytes(4096, 64) >= 64 * 64 * 8
+    assert lib.spion_attn_workspace_bytes(128, 4096, 64, N.BF16) >= 128 * 4096 * 64 * 4
+    assert lib.spion_step_arena_bytes(2, 64, 16, 8, N.F32) > 0
+
+
+def _bsr_dummy(L, B):
+    s = N.BSR()
+    fake = 256  # never dereferenced: validation fails first
+    s.brow_ptr = s.bcol_idx = s.bcol_ptr = s.brow_idx = s.nnzb = fake
+    s.nnzb_cap = (L // B) ** 2
+    return s
+
+
+@pytest.mark.parametrize("L,B,F,theta,kind,want", [
+    (100, 64, 31, 90.0, 0, 1),      # L % B -> shape
+    (0, 8, 31, 90.0, 0, 1),
+    (64, 8, 30, 90.0, 0, 2),        # even filter -> param
+    (64, 8, 31, 100.0, 0, 2),       # alpha outside (0,100)
+    (64, 8, 31, 0.0, 1, 2),
+    (64, 8, 31, float("nan"), 2, 2),
+    (64, 8, 31, 90.0, 9, 2),        # bad enum
+    (64 * 256, 8, 31, 90.0, 0, 7),  # nblk > 128 -> unsupported
+])
+def test_pattern_rejects_bad_arguments(L, B, F, theta, kind, want):
+    lib = N.lib()
+    s = _bsr_dummy(max(L, 1), B)
+    st = lib.spion_pattern(ctypes.c_void_p(256), L, B, F, theta, kind, ctypes.c_void_p(256), 1 << 30,
+                           ctypes.byref(s), None, None)
+    assert st == want
+
+
+def test_pattern_rejects_misaligned_and_small_workspace():
+    lib = N.lib()
+    s = _bsr_dummy(64, 8)
+    assert lib.spion_pattern(ctypes.c_void_p(258), 64, 8, 31, 90.0, 0, ctypes.c_void_p(256), 1 << 30,
+                             ctypes.byref(s), None, None) == 4
+    assert lib.spion_pattern(ctypes.c_void_p(256), 64, 8, 31, 90.0, 0, ctypes.c_void_p(256), 8,
+                             ctypes.byref(s), None, None) == 5
+
+
+def test_attention_rejects_bad_arguments():
+    lib = N.lib()
+    s = _bsr_dummy(64, 8)
+    s.L, s.block, s.nblk = 64, 8, 8
+    P = ctypes.c_void_p(256)
+    # d > 128
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 256, 64 * 256, 256, N.F32, ctypes.byref(s), 0, 1.0, None) == 1
+    # pattern for another L
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 128, 16, 128 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0, None) == 1
+    # bad mode / dtype
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 5, 1.0, None) == 2
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, 7, ctypes.byref(s), 0, 1.0, None) == 2
+    # misaligned stride for bf16
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 20, 20, N.BF16, ctypes.byref(s), 0, 1.0, None) == 4
+    # workspace too small
+    assert lib.spion_attn_bwd(P, P, P, P, P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0,
+                              P, 16, None) == 5
+
+
+def test_status_strings():
+    lib = N.lib()
+    for k in range(8):
+        assert lib.spion_status_str(k)

@@ -1,0 +1,109 @@
+"""GPU parity of pattern generation (K1 stencil + K2 finalize) against the oracle.
+
+Bar: bit-exact block mask, block-CSR, block-CSC and nnzb (integer work).
+Sizes: the tiny config, every LRA shape of BASELINE.json at the paper's alpha
+and at alpha=75, plus ragged / degenerate cases.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _spion():
+    from paper_2309_12578_b200 import spion
+    return spion
+
+
+def _check(bp, fl_ref):
+    n = fl_ref.shape[0]
+    ref = oracle.mask_to_bsr(fl_ref)
+    assert (bp.mask.view(n, n).cpu().numpy() == fl_ref).all()
+    assert bp.nnzb == ref["nnzb"]
+    rp, ci = bp.csr()
+    cp, ri = bp.csc()
+    assert (rp.cpu().numpy() == ref["brow_ptr"]).all()
+    assert (ci.cpu().numpy() == ref["bcol_idx"]).all()
+    assert (cp.cpu().numpy() == ref["bcol_ptr"]).all()
+    assert (ri.cpu().numpy() == ref["brow_idx"]).all()
+
+
+CASES = [
+    # L, B, F, theta, kind
+    (64, 8, 31, 0.1, "absolute"),        # tiny config, fixed threshold
+    (64, 8, 31, 75.0, "linear"),
+    (1024, 32, 31, 96.0, "linear"),      # LRA Image, paper alpha
+    (1024, 32, 31, 75.0, "linear"),
+    (2048, 64, 31, 98.0, "linear"),      # ListOps
+    (2048, 64, 31, 75.0, "linear"),
+    (4096, 64, 31, 99.0, "linear"),      # Text / Retrieval
+    (4096, 64, 31, 75.0, "linear"),
+    (4096, 32, 31, 90.0, "linear"),      # nblk = 128 (largest supported)
+    (1024, 32, 31, 96.0, "nearest"),
+    (256, 16, 1, 80.0, "linear"),        # SPION-F (no conv) == F=1
+    (256, 16, 3, 50.0, "linear"),
+    (192, 64, 31, 50.0, "linear"),       # nblk = 3
+    (64, 64, 31, 50.0, "linear"),        # nblk = 1
+    (96, 4, 63, 60.0, "linear"),         # h > B (targets span several pool rows)
+    (1024, 32, 31, 0.05, "absolute"),
+]
+
+
+@pytest.mark.parametrize("L,B,F,theta,kind", CASES)
+def test_pattern_bit_exact(L, B, F, theta, kind):
+    spion = _spion()
+    A = synth.syn_scores(L, B, heads=2, seed=L + B + F)
+    bp = spion.pattern(A.to(DEV), B, filter=F, alpha=None if kind == "absolute" else theta,
+                       t=theta if kind == "absolute" else None, kind=kind, sync=True)
+    fl_ref, _, _ = oracle.pattern(A.numpy(), B, F, theta, kind)
+    _check(bp, fl_ref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pattern_random_scores_with_ties(seed):
+    """Quantised values with heavy ties exercise the ==m edges and the order statistics."""
+    spion = _spion()
+    rng = np.random.default_rng(seed)
+    L, B = 256, 16
+    A = (rng.integers(0, 4, size=(L, L)) / 3.0).astype(np.float32)
+    for alpha in (10.0, 50.0, 90.0, 99.0):
+        bp = spion.pattern(torch.from_numpy(A).to(DEV), B, filter=7, alpha=alpha, sync=True)
+        fl_ref, _, _ = oracle.pattern(A, B, 7, alpha)
+        _check(bp, fl_ref)
+
+
+def test_pattern_flags_bad_scores():
+    spion = _spion()
+    from paper_2309_12578_b200 import _native as N
+    A = synth.syn_scores(128, 16, heads=1, seed=3)
+    A[5, 7] = float("nan")
+    with pytest.raises(N.SpionError) as e:
+        spion.pattern(A.to(DEV), 16, filter=31, alpha=90.0, sync=True)
+    assert e.value.status == 3
+
+
+@pytest.mark.parametrize("n,density,seed", [(8, 0.3, 0), (32, 0.1, 1), (64, 0.1, 2), (128, 0.05, 3), (5, 0.5, 4)])
+def test_bsr_from_mask_matches_oracle(n, density, seed):
+    spion = _spion()
+    m = synth.syn_mask(n, density, seed)
+    rng = np.random.default_rng(seed)
+    if n > 4:
+        m[rng.integers(0, n)] = 0  # an empty row (user masks only)
+    bp = spion.bsr_from_mask(torch.from_numpy(m).to(DEV), n * 32, 32)
+    _check(bp, m)
+
+
+def test_bsr_from_mask_rejects_non_binary():
+    spion = _spion()
+    from paper_2309_12578_b200 import _native as N
+    m = np.eye(8, dtype=np.uint8)
+    m[2, 3] = 2
+    with pytest.raises(N.SpionError) as e:
+        spion.bsr_from_mask(torch.from_numpy(m).to(DEV), 256, 32)
+    assert e.value.status == 3
