@@ -53,7 +53,71 @@ struct TcParams {
     int mode;
     float scale, scale_log2;
     int off_ptr, off_col, off_msk;  // plan word offsets (fwd: fptr/fcol/fmsk, bwd: bptr/brow/bmsk)
+    int off_order;                  // tiles in descending work order
+    int off_sched;                  // plan words [off_sched] item counter, [off_sched+1] done counter
+    int G;                          // (batch, head) chunk of the scheduling order
 };
+
+// ---------------------------------------------------------------- dynamic tile scheduler
+// Items (bh, tile) are handed out by an atomic counter in the plan, in chunks of G
+// (batch, head): within a chunk, tiles in descending order of work (plan order
+// list), each for all G bh.  The producer warp fetches an item and broadcasts it
+// through a 4-slot shared-memory ring to the MMA thread and the 4 softmax warps.
+// The last CTA to finish resets the counters, so every launch starts from zero.
+struct Sched {
+    int *item;        // [4]
+    uint64_t *full;   // [4], count 1
+    uint64_t *empty;  // [4], count 5 (MMA thread + 4 softmax warps)
+};
+
+__device__ __forceinline__ int sched_produce(const Sched &sc, int k, int *counter, int nitems) {
+    const int slot = k & 3;
+    const uint32_t ph = (k >> 2) & 1;
+    mbar_wait(sc.empty + slot, ph ^ 1);
+    int item = atomicAdd(counter, 1);
+    if (item >= nitems) item = -1;
+    *reinterpret_cast<volatile int *>(sc.item + slot) = item;
+    mbar_arrive(sc.full + slot);
+    return item;
+}
+
+// whole_warp: all 32 lanes call (one arrival by lane 0 after the warp has read the slot);
+// otherwise a single thread calls and arrives.
+__device__ __forceinline__ int sched_consume(const Sched &sc, int k, bool whole_warp) {
+    const int slot = k & 3;
+    const uint32_t ph = (k >> 2) & 1;
+    mbar_wait(sc.full + slot, ph);
+    const int item = *reinterpret_cast<volatile int *>(sc.item + slot);
+    if (whole_warp) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(sc.empty + slot);
+    } else {
+        mbar_arrive(sc.empty + slot);
+    }
+    return item;
+}
+
+__device__ __forceinline__ void decode_item(int item, const TcParams &p, int &bh, int &t) {
+    const int per = p.G * p.ntiles;
+    const int c = item / per;
+    const int rem = item - c * per;
+    const int Gc = min(p.G, (int)p.bh - c * p.G);
+    const int k = rem / Gc;
+    bh = c * p.G + (rem - k * Gc);
+    t = p.plan[p.off_order + k];
+}
+
+__device__ __forceinline__ void sched_finish(const TcParams &p) {
+    if (threadIdx.x == 0) {
+        int *ctr = const_cast<int *>(p.plan) + p.off_sched;
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(ctr, 0);
+            atomicExch(ctr + 1, 0);
+            __threadfence();
+        }
+    }
+}
 
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
     return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -80,6 +144,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
              *tmem_free = bars + 4, *s_full = bars + 5 /*[2]*/, *kv_full = bars + 7 /*[NST]*/,
              *kv_empty = bars + 7 + FWD_NST /*[NST]*/;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 7 + 2 * FWD_NST);
+    Sched sc{reinterpret_cast<int *>(bars + 7 + 2 * FWD_NST + 1), bars + 7 + 2 * FWD_NST + 3, bars + 7 + 2 * FWD_NST + 7};
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -91,6 +156,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         mbar_init(s_full + 0, 1);
         mbar_init(s_full + 1, 1);
         for (int i = 0; i < FWD_NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+        for (int i = 0; i < 4; ++i) { mbar_init(sc.full + i, 1); mbar_init(sc.empty + i, 5); }
         fence_barrier_init();
     }
     if (warp == 5) tmem_alloc<256>(tmem_slot);
@@ -110,8 +176,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             int st = 0;
             uint32_t ph = 0;
             int nq = 0;
-            for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int bh = (int)(item / p.ntiles), t = (int)(item % p.ntiles);
+            int *counter = const_cast<int *>(plan) + p.off_sched;
+            for (int ks = 0;; ++ks) {
+                const int item = sched_produce(sc, ks, counter, (int)nitems);
+                if (item < 0) break;
+                int bh, t;
+                decode_item(item, p, bh, t);
                 const int beg = plan[p.off_ptr + t], end = plan[p.off_ptr + t + 1];
                 if (end == beg) continue;
                 if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);
@@ -136,8 +206,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             int nq = 0;
             const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ));
             const uint64_t dP0 = sdesc_sw128(smem_u32(sP));
-            for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int t = (int)(item % p.ntiles);
+            for (int ks = 0;; ++ks) {
+                const int item = sched_consume(sc, ks, false);
+                if (item < 0) break;
+                int bh, t;
+                decode_item(item, p, bh, t);
                 const int beg = plan[p.off_ptr + t], end = plan[p.off_ptr + t + 1];
                 const int cnt = end - beg;
                 if (cnt == 0) continue;
@@ -184,8 +257,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         uint32_t sph0 = 0, sph1 = 0, pv_ph = 0;
         const float sl2 = p.scale_log2;
         __nv_bfloat16 *Obase = static_cast<__nv_bfloat16 *>(p.O);
-        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-            const int bh = (int)(item / p.ntiles), t = (int)(item % p.ntiles);
+        for (int ks = 0;; ++ks) {
+            const int item = sched_consume(sc, ks, true);
+            if (item < 0) break;
+            int bh, t;
+            decode_item(item, p, bh, t);
             const int beg = plan[p.off_ptr + t], end = plan[p.off_ptr + t + 1];
             const int cnt = end - beg;
             const int I = t * S + slot;
@@ -314,6 +390,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         }
     }
     __syncthreads();
+    sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
         tmem_dealloc<256>(tmem);
@@ -372,6 +449,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
              *dq_full = bars + 4, *dq_free = bars + 5, *q_full = bars + 6 /*[NST]*/,
              *q_empty = bars + 6 + BWD_NST /*[NST]*/;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6 + 2 * BWD_NST);
+    Sched sc{reinterpret_cast<int *>(bars + 6 + 2 * BWD_NST + 1), bars + 6 + 2 * BWD_NST + 3, bars + 6 + 2 * BWD_NST + 7};
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -382,6 +460,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         mbar_init(dq_full, 1);
         mbar_init(dq_free, 128);
         for (int i = 0; i < BWD_NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
+        for (int i = 0; i < 4; ++i) { mbar_init(sc.full + i, 1); mbar_init(sc.empty + i, 5); }
         fence_barrier_init();
     }
     if (warp == 5) tmem_alloc<256>(tmem_slot);
@@ -402,8 +481,12 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
             int st = 0;
             uint32_t ph = 0;
             int nk = 0;
-            for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int bh = (int)(item / p.ntiles), t = (int)(item % p.ntiles);
+            int *counter = const_cast<int *>(plan) + p.off_sched;
+            for (int ks = 0;; ++ks) {
+                const int item = sched_produce(sc, ks, counter, (int)nitems);
+                if (item < 0) break;
+                int bh, t;
+                decode_item(item, p, bh, t);
                 const int beg = plan[p.off_ptr + t], end = plan[p.off_ptr + t + 1];
                 if (end == beg) continue;
                 if (nk > 0) mbar_wait(kv_empty, (nk - 1) & 1);
@@ -435,8 +518,11 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
             const uint64_t dV0 = sdesc_sw128(smem_u32(sV));
             const uint64_t dPt0 = sdesc_sw128(smem_u32(sPt));
             const uint64_t ddSt0 = sdesc_sw128(smem_u32(sdSt));
-            for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int t = (int)(item % p.ntiles);
+            for (int ks = 0;; ++ks) {
+                const int item = sched_consume(sc, ks, false);
+                if (item < 0) break;
+                int bh, t;
+                decode_item(item, p, bh, t);
                 const int beg = plan[p.off_ptr + t], end = plan[p.off_ptr + t + 1];
                 const int cnt = end - beg;
                 if (cnt == 0) continue;
@@ -488,8 +574,11 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         int st = 0;
         uint32_t ph = 0;
         const float sl2 = p.scale_log2;
-        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-            const int bh = (int)(item / p.ntiles), t = (int)(item % p.ntiles);
+        for (int ks = 0;; ++ks) {
+            const int item = sched_consume(sc, ks, true);
+            if (item < 0) break;
+            int bh, t;
+            decode_item(item, p, bh, t);
             const int beg = plan[p.off_ptr + t], end = plan[p.off_ptr + t + 1];
             const int cnt = end - beg;
             const int key = t * 128 + r;
@@ -601,6 +690,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         }
     }
     __syncthreads();
+    sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
         tmem_dealloc<256>(tmem);
@@ -643,6 +733,7 @@ bool tc_supported(const AttnArgs &a, spion_dtype dt) {
     return !disabled && get_encode() != nullptr;
 }
 
+
 static int num_sms() {
     static int n = 0;
     if (!n) {
@@ -672,6 +763,13 @@ static TcParams base_params(const AttnArgs &a, bool fwd) {
     p.off_ptr = (int)(fwd ? pl.fptr : pl.bptr);
     p.off_col = (int)(fwd ? pl.fcol : pl.brow);
     p.off_msk = (int)(fwd ? pl.fmsk : pl.bmsk);
+    p.off_order = (int)(fwd ? pl.forder : pl.border);
+    p.off_sched = fwd ? 8 : 10;
+    const int grid = 2 * num_sms();
+    int G = (2 * grid + pl.ntiles - 1) / pl.ntiles;
+    if (G < 1) G = 1;
+    if (G > a.bh) G = (int)a.bh;
+    p.G = G;
     return p;
 }
 

@@ -90,17 +90,21 @@ __device__ __forceinline__ int warp_excl_scan_i32(int v, int lane) {
 // ---- plan layout (int32 words; see pattern.cu)
 struct PlanLayout {
     int n, S, ntiles;
-    size_t fptr, bptr, fcol, fmsk, brow, bmsk, words;
+    // header words: [0] n [1] S [2] ntiles [3] fwd entries [4] bwd entries
+    //               [8] fwd item counter [9] fwd done [10] bwd item counter [11] bwd done
+    size_t fptr, bptr, forder, border, fcol, fmsk, brow, bmsk, words;
     __host__ __device__ PlanLayout(int n_, int block) {
         n = n_;
         S = block >= 128 ? 1 : 128 / block;
         if (S > 32) S = 32;
         if (S < 1) S = 1;
         ntiles = (n + S - 1) / S;
-        fptr = 8;
+        fptr = 16;
         bptr = fptr + ntiles + 1;
+        forder = bptr + ntiles + 1;
+        border = forder + ntiles;
         size_t cap = (size_t)n * ntiles;
-        fcol = bptr + ntiles + 1;
+        fcol = border + ntiles;
         fmsk = fcol + cap;
         brow = fmsk + cap;
         bmsk = brow + cap;

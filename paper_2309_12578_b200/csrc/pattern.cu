@@ -262,9 +262,23 @@ __device__ void build_bsr_and_plan(const uint8_t *fl, int n, int block, int *bro
                 for (int q = 0; q < per; ++q) { int r = tid * per + q; if (r < pl.ntiles) { ptr[r] = ex; s_off[which * (pl.ntiles + 1) + r] = ex; ex += cnt[r]; } }
                 if (tid == 31) { ptr[pl.ntiles] = ex; plan[3 + which] = ex; }
             }
-            if (tid == 0) { plan[0] = n; plan[1] = pl.S; plan[2] = pl.ntiles; }
+            if (tid == 0) {
+                plan[0] = n; plan[1] = pl.S; plan[2] = pl.ntiles;
+                for (int w = 5; w < 16; ++w) plan[w] = 0;  // scheduler counters start at zero
+            }
         }
         __syncthreads();
+        // tiles in descending order of work (stable): the attention kernels hand out the
+        // longest tiles of a bh-chunk first (longest-processing-time-first scheduling)
+        for (int t = tid; t < 2 * pl.ntiles; t += blockDim.x) {
+            const bool fwd = t < pl.ntiles;
+            const int tt = fwd ? t : t - pl.ntiles;
+            const int *cnt = s_cnt + (fwd ? 0 : pl.ntiles);
+            const int c = cnt[tt];
+            int rank = 0;
+            for (int u = 0; u < pl.ntiles; ++u) rank += (cnt[u] > c) || (cnt[u] == c && u < tt);
+            plan[(fwd ? pl.forder : pl.border) + rank] = tt;
+        }
         for (int t = tid; t < 2 * pl.ntiles; t += blockDim.x) {
             const bool fwd = t < pl.ntiles;
             const int tt = fwd ? t : t - pl.ntiles;
