@@ -134,8 +134,9 @@ SPION_API spion_status spion_pattern_check(const void *ws_dev, int32_t *flags_ho
 SPION_API spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t block, spion_bsr *out,
                                  int32_t *nnzb_host, void *stream);
 
-/* Bytes of device workspace spion_attn_bwd needs: fp32 dQ accumulator
- * [bh][L][d] and D_i = rowsum(dO*O) [bh][L].  spion_attn_fwd needs none. */
+/* Bytes of device workspace spion_attn_bwd needs: D_i = rowsum(dO*O), fp32
+ * [bh][L] (the backward is atomic-free and deterministic).  spion_attn_fwd
+ * needs none. */
 SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt);
 
 /* Forward block-sparse attention, per (batch, head) b (Alg. 5 l.4-8,

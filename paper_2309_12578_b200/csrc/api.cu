@@ -160,7 +160,7 @@ spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t blo
 size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt) {
     (void)dt;
     if (bh <= 0 || L <= 0 || d <= 0) return 0;
-    return round_up((size_t)bh * L * d * 4, 256) + round_up((size_t)bh * L * 4, 256);
+    return round_up((size_t)bh * L * 4, 256);  // D_i = rowsum(dO * O), fp32
 }
 
 static spion_status check_attn_common(const void *Q, const void *K, const void *V, int64_t bh, int32_t L,
@@ -241,8 +241,7 @@ spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_
     a.dQ = dQ_dev;
     a.dK = dK_dev;
     a.dV = dV_dev;
-    a.dQacc = static_cast<float *>(ws_dev);
-    float *D = reinterpret_cast<float *>(static_cast<char *>(ws_dev) + round_up((size_t)bh * L * d * 4, 256));
+    float *D = static_cast<float *>(ws_dev);
     a.D = D;
     if (dt == SPION_BF16 && tc_supported(a, dt)) return launch_bwd_tc(a, s);
     if (!simt_supported(a.B, d)) return SPION_ERR_UNSUPPORTED;

@@ -9,7 +9,6 @@ struct AttnArgs {
     void *Oout, *dQ, *dK, *dV;
     float *lse_out;
     const float *lse, *D;
-    float *dQacc;  // fp32 [bh][L][d] workspace (tensor-core backward)
     int64_t bh, stride_bh, stride_l;
     int L, d, B, n;
     int mode;
