@@ -38,9 +38,13 @@ namespace spion {
 using namespace tc;
 
 static constexpr int TC_THREADS = 192;
-static constexpr int FWD_NST = 3;   // K/V ring stages (forward)
-static constexpr int DQ_NST = 2;    // K/V ring stages (dQ)
-static constexpr int DKV_NST = 2;   // Q/dO/lse/D ring stages (dK/dV)
+// ring stages: as many as fit next to the fixed tiles with 2 CTAs per SM (~104 KB each);
+// a B=32 stage is half the size of a B=64 one, so it gets twice the depth
+template <int B> struct Stages {
+    static constexpr int FWD = B == 32 ? 8 : 4;  // K_J + V_J per stage
+    static constexpr int DQ = B == 32 ? 6 : 3;   // K_J + V_J per stage
+    static constexpr int DKV = B == 32 ? 4 : 2;  // Q_I + dO_I + lse_I + D_I per stage
+};
 static constexpr int SCHED_CAP = 128;  // max entries of one tile list (nblk <= 128)
 static constexpr float LOG2E = 1.4426950408889634f;
 static constexpr float LN2 = 0.6931471805599453f;
@@ -183,6 +187,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, TcParams p) {
     constexpr uint32_t KV_BYTES = B * 128;
+    constexpr int FWD_NST = Stages<B>::FWD;
+    constexpr uint32_t STG = 2 * KV_BYTES;  // K at +0, V at +KV_BYTES
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, 64, false, true);
     constexpr uint32_t COL_S = 0, COL_O = 128;
@@ -191,8 +197,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sQ = smem;
     uint8_t *sP = smem + 16384;
-    uint8_t *sKV = smem + 32768;  // stage st: K at st*16384, V at st*16384 + 8192
-    uint8_t *sSched = sKV + FWD_NST * 16384;
+    uint8_t *sKV = smem + 32768;  // stage st: K at st*STG, V at st*STG + KV_BYTES
+    uint8_t *sSched = sKV + FWD_NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
     uint64_t *q_full = bars + 0, *q_empty = bars + 1, *p_full = bars + 2, *pv_done = bars + 3,
              *s_full = bars + 4 /*[2]*/, *kv_full = bars + 6 /*[NST]*/, *kv_empty = bars + 6 + FWD_NST /*[NST]*/;
@@ -237,8 +243,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
                     mbar_arrive_expect_tx(kv_full + st, 2 * KV_BYTES);
-                    tma_load_3d(sKV + st * 16384, &tmK, kv_full + st, 0, col[j] * B, bh);
-                    tma_load_3d(sKV + st * 16384 + 8192, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                    tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
                     if (++st == FWD_NST) { st = 0; ph ^= 1; }
                 }
             }
@@ -266,7 +272,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                             mbar_wait(kv_full + st, ph);
                             tc_fence_after();
                             const uint32_t sb = jj & 1;
-                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * 16384));
+                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_bf16_ss(tmem + COL_S + sb * 64, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
@@ -278,7 +284,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                             mbar_wait(p_full, p_ph);
                             p_ph ^= 1;
                             tc_fence_after();
-                            const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + prev_st * 16384 + 8192));
+                            const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + prev_st * STG + KV_BYTES));
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
                                 mma_bf16_ss(tmem + COL_O, dP0 + 2 * k, dV0 + 128 * k, IDESC_PV, (jj > 1) || (k > 0));
@@ -424,15 +430,18 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, TcParams p) {
     constexpr uint32_t KV_BYTES = B * 128;
+    constexpr int DQ_NST = Stages<B>::DQ;
+    constexpr uint32_t STG = 2 * KV_BYTES;
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);   // S = Q K^T, dP = dO V^T
     constexpr uint32_t IDESC_DQ = idesc_bf16(128, 64, false, true);  // dQ = dS K
     constexpr uint32_t COL_S = 0, COL_DP = 64, COL_DQ = 128;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *sQ = smem, *sdO = smem + 16384, *sO = smem + 32768, *sdS = smem + 49152;
-    uint8_t *sKV = smem + 65536;  // stage st: K at st*16384, V at +8192
-    uint8_t *sSched = sKV + DQ_NST * 16384;
+    // O is staged in the dS buffer: it is only read (for D) before the first dS is written
+    uint8_t *sQ = smem, *sdO = smem + 16384, *sdS = smem + 32768, *sO = sdS;
+    uint8_t *sKV = smem + 49152;  // stage st: K at st*STG, V at +KV_BYTES
+    uint8_t *sSched = sKV + DQ_NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
     uint64_t *q_full = bars + 0, *q_empty = bars + 1, *s_full = bars + 2, *ds_full = bars + 3,
              *dq_full = bars + 4, *kv_full = bars + 5 /*[NST]*/, *kv_empty = bars + 5 + DQ_NST /*[NST]*/;
@@ -480,8 +489,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
                     mbar_arrive_expect_tx(kv_full + st, 2 * KV_BYTES);
-                    tma_load_3d(sKV + st * 16384, &tmK, kv_full + st, 0, col[j] * B, bh);
-                    tma_load_3d(sKV + st * 16384 + 8192, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                    tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
                     if (++st == DQ_NST) { st = 0; ph ^= 1; }
                 }
             }
@@ -505,8 +514,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                     for (int jj = 0; jj < cnt; ++jj) {
                         mbar_wait(kv_full + st, ph);
                         tc_fence_after();
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * 16384));
-                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * 16384 + 8192));
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
+                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * STG + KV_BYTES));
 #pragma unroll
                         for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + COL_S, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
 #pragma unroll
@@ -621,32 +630,35 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 }
 
 // ============================================================================ backward: dK, dV
+// K/V tiles are double buffered across items; P^T and dS^T never leave the SM:
+// they are written as packed bf16 over the S^T / dP^T columns of TMEM and feed
+// the dV / dK MMAs as the A operand straight from tensor memory.
 template <int B>
 __global__ void __launch_bounds__(TC_THREADS, 2)
 attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         TcParams p) {
     constexpr uint32_t TILE = B * 128;
+    constexpr int DKV_NST = Stages<B>::DKV;
+    constexpr uint32_t STAGE = 2 * TILE + 1024;  // Q_I, dO_I, lse_I, D_I
     constexpr uint32_t IDESC_ST = idesc_bf16(128, B, false, false);   // S^T = K Q^T, dP^T = V dO^T
     constexpr uint32_t IDESC_DKV = idesc_bf16(128, 64, false, true);  // dV += P^T dO, dK += dS^T Q
-    constexpr uint32_t COL_S = 0, COL_DP = 64, COL_DV = 128, COL_DK = 192;
-    constexpr uint32_t STAGE = 2 * 8192 + 1024;  // Q_I, dO_I (<= 8 KB each), lse_I, D_I
+    constexpr uint32_t COL_S = 0, COL_DP = 64, COL_DV = 128, COL_DK = 192;  // P^T over S^T, dS^T over dP^T
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *sK = smem, *sV = smem + 16384, *sPt = smem + 32768, *sdSt = smem + 49152;
+    uint8_t *sKV = smem;  // buffer kb: K at kb*32768, V at kb*32768 + 16384
     uint8_t *sStage = smem + 65536;
     uint8_t *sSched = sStage + DKV_NST * STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *kv_full = bars + 0, *kv_empty = bars + 1, *s_full = bars + 2, *p_full = bars + 3,
-             *acc_full = bars + 4, *q_full = bars + 5 /*[NST]*/, *q_empty = bars + 5 + DKV_NST /*[NST]*/;
-    Sched sc = make_sched(sSched, bars + 5 + 2 * DKV_NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5 + 2 * DKV_NST + 8);
+    uint64_t *kv_full = bars + 0 /*[2]*/, *kv_empty = bars + 2 /*[2]*/, *s_full = bars + 4, *p_full = bars + 5,
+             *acc_full = bars + 6, *q_full = bars + 7 /*[NST]*/, *q_empty = bars + 7 + DKV_NST /*[NST]*/;
+    Sched sc = make_sched(sSched, bars + 7 + 2 * DKV_NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 7 + 2 * DKV_NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        mbar_init(kv_full, 1);
-        mbar_init(kv_empty, 1);
+        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         mbar_init(s_full, 1);
         mbar_init(p_full, 128);
         mbar_init(acc_full, 1);
@@ -672,10 +684,11 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *rows = sc.col + (ks & 3) * SCHED_CAP;
             if (lane == 0 && cnt > 0) {
-                if (nk > 0) mbar_wait(kv_empty, (nk - 1) & 1);
-                mbar_arrive_expect_tx(kv_full, 32768);
-                tma_load_3d(sK, &tmK, kv_full, 0, t * 128, bh);
-                tma_load_3d(sV, &tmV, kv_full, 0, t * 128, bh);
+                const int kb = nk & 1;
+                if (nk >= 2) mbar_wait(kv_empty + kb, ((nk >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(kv_full + kb, 32768);
+                tma_load_3d(sKV + kb * 32768, &tmK, kv_full + kb, 0, t * 128, bh);
+                tma_load_3d(sKV + kb * 32768 + 16384, &tmV, kv_full + kb, 0, t * 128, bh);
                 ++nk;
                 for (int j = 0; j < cnt; ++j) {
                     const int I = rows[j];
@@ -683,9 +696,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     uint8_t *stg = sStage + st * STAGE;
                     mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
                     tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
-                    tma_load_3d(stg + 8192, &tmdO, q_full + st, 0, I * B, bh);
-                    bulk_load(stg + 16384, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
-                    bulk_load(stg + 16384 + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                    tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
+                    bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                    bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
                     if (++st == DKV_NST) { st = 0; ph ^= 1; }
                 }
             }
@@ -695,41 +708,41 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         if (lane == 0) {
             int st = 0, nk = 0;
             uint32_t ph = 0, p_ph = 0;
-            const uint64_t dK0 = sdesc_sw128(smem_u32(sK));
-            const uint64_t dV0 = sdesc_sw128(smem_u32(sV));
-            const uint64_t dPt0 = sdesc_sw128(smem_u32(sPt));
-            const uint64_t ddSt0 = sdesc_sw128(smem_u32(sdSt));
             for (int ks = 0;; ++ks) {
                 const int *h = sched_wait(sc, ks);
                 if (h[0] < 0) break;
                 const int cnt = h[3];
                 if (cnt > 0) {
-                    mbar_wait(kv_full, nk & 1);
+                    const int kb = nk & 1;
+                    mbar_wait(kv_full + kb, (nk >> 1) & 1);
                     tc_fence_after();
                     ++nk;
+                    const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
+                    const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
                     for (int jj = 0; jj < cnt; ++jj) {
                         mbar_wait(q_full + st, ph);
                         tc_fence_after();
                         uint8_t *stg = sStage + st * STAGE;
                         const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
-                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + 8192));
+                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
 #pragma unroll
                         for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + COL_S, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             mma_bf16_ss(tmem + COL_DP, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
                         mma_commit(s_full);
+                        if (jj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
                         mbar_wait(p_full, p_ph);
                         p_ph ^= 1;
                         tc_fence_after();
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ss(tmem + COL_DV, dPt0 + 2 * k, ddO0 + 128 * k, IDESC_DKV, (jj > 0) || (k > 0));
+                            mma_bf16_ts(tmem + COL_DV, tmem + COL_S + 8 * k, ddO0 + 128 * k, IDESC_DKV, (jj > 0) || (k > 0));
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ss(tmem + COL_DK, ddSt0 + 2 * k, dQ0 + 128 * k, IDESC_DKV, (jj > 0) || (k > 0));
+                            mma_bf16_ts(tmem + COL_DK, tmem + COL_DP + 8 * k, dQ0 + 128 * k, IDESC_DKV, (jj > 0) || (k > 0));
                         mma_commit(q_empty + st);
-                        if (jj == cnt - 1) { mma_commit(acc_full); mma_commit(kv_empty); }
+                        if (jj == cnt - 1) mma_commit(acc_full);
                         if (++st == DKV_NST) { st = 0; ph ^= 1; }
                     }
                 }
@@ -737,7 +750,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             }
         }
     } else {
-        const int r = threadIdx.x;  // key row of the tile
+        const int r = threadIdx.x;  // key row of the tile = TMEM lane
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
         uint32_t s_ph = 0, a_ph = 0, ph = 0;
@@ -762,9 +775,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;
                 mbar_wait(q_full + st, ph);
-                const float *slse = reinterpret_cast<const float *>(sStage + st * STAGE + 16384);
+                const float *slse = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
                 const float *sD = slse + 128;
-                mbar_wait(s_full, s_ph);  // also implies dV/dK(jj-1) finished reading sPt/sdSt
+                mbar_wait(s_full, s_ph);
                 s_ph ^= 1;
                 tc_fence_after();
 #pragma unroll
@@ -787,15 +800,11 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
 #pragma unroll
                         for (int i = 0; i < 16; ++i) { pk[i] = 0u; dk[i] = 0u; }
                     }
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        *reinterpret_cast<uint4 *>(sPt + sw128_offset(r, hh * 4 + c)) =
-                            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-                        *reinterpret_cast<uint4 *>(sdSt + sw128_offset(r, hh * 4 + c)) =
-                            make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
-                    }
+                    // packed bf16 P^T / dS^T over the (already read) S^T / dP^T columns
+                    tmem_st16(tl + COL_S + hh * 16, pk);
+                    tmem_st16(tl + COL_DP + hh * 16, dk);
                 }
-                fence_proxy_async_smem();
+                tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(p_full);
                 if (++st == DKV_NST) { st = 0; ph ^= 1; }
@@ -906,9 +915,9 @@ static TcParams base_params(const AttnArgs &a, int which) {
 }
 
 static const size_t SCHED_AREA = SCHED_BYTES + 256;
-static const size_t FWD_SMEM = 1024 + 32768 + FWD_NST * 16384 + SCHED_AREA;
-static const size_t DQ_SMEM = 1024 + 65536 + DQ_NST * 16384 + SCHED_AREA;
-static const size_t DKV_SMEM = 1024 + 65536 + DKV_NST * (2 * 8192 + 1024) + SCHED_AREA;
+template <int B> static size_t fwd_smem() { return 1024 + 32768 + Stages<B>::FWD * 2 * B * 128 + SCHED_AREA; }
+template <int B> static size_t dq_smem() { return 1024 + 49152 + Stages<B>::DQ * 2 * B * 128 + SCHED_AREA; }
+template <int B> static size_t dkv_smem() { return 1024 + 65536 + Stages<B>::DKV * (2 * B * 128 + 1024) + SCHED_AREA; }
 
 static int grid_for(const TcParams &p) {
     const int64_t items = p.bh * p.ntiles;
@@ -919,7 +928,7 @@ template <int B>
 static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FWD_SMEM));
+        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem<B>()));
         attr = true;
     }
     CUtensorMap mq, mk, mv;
@@ -930,7 +939,7 @@ static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     TcParams p = base_params(a, 0);
     p.O = a.Oout;
     p.lse_out = a.lse_out;
-    attn_fwd_tc_kernel<B><<<grid_for(p), TC_THREADS, FWD_SMEM, s>>>(mq, mk, mv, p);
+    attn_fwd_tc_kernel<B><<<grid_for(p), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, p);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
@@ -939,8 +948,8 @@ template <int B>
 static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DQ_SMEM));
-        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DKV_SMEM));
+        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dq_smem<B>()));
+        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dkv_smem<B>()));
         attr = true;
     }
     CUtensorMap mq128, mdo128, mo128, mkB, mvB, mk128, mv128, mqB, mdoB;
@@ -960,7 +969,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     p.lse = a.lse;
     p.D = const_cast<float *>(a.D);
     p.dQ = a.dQ;
-    attn_bwd_dq_tc_kernel<B><<<grid_for(p), TC_THREADS, DQ_SMEM, s>>>(mq128, mdo128, mo128, mkB, mvB, p);
+    attn_bwd_dq_tc_kernel<B><<<grid_for(p), TC_THREADS, dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, p);
     SPION_LAUNCH_CHECK();
     // 2) dK, dV (column tiles)
     TcParams q = base_params(a, 2);
@@ -968,7 +977,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     q.D = const_cast<float *>(a.D);
     q.dK = a.dK;
     q.dV = a.dV;
-    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q), TC_THREADS, DKV_SMEM, s>>>(mk128, mv128, mqB, mdoB, q);
+    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q), TC_THREADS, dkv_smem<B>(), s>>>(mk128, mv128, mqB, mdoB, q);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
