@@ -26,6 +26,17 @@ extern "C" {
 
 int64_t spion_launch_count(void) { return (int64_t)g_launches.load(); }
 
+// debug: copy the event trace of the last traced kernel (SPION_TRACE=1) to host:
+// 3 roles (producer, MMA, softmax thread 0) x 1024 (event, globaltimer) pairs
+SPION_API int64_t spion_debug_trace(unsigned long long *host, int64_t cap) {
+    if (!spion::g_trace_buf) return 0;
+    cudaDeviceSynchronize();
+    int64_t n = 3 * 2048;
+    if (n > cap) n = cap;
+    cudaMemcpy(host, spion::g_trace_buf + 16, n * 8, cudaMemcpyDeviceToHost);
+    return n;
+}
+
 const char *spion_status_str(spion_status s) {
     switch (s) {
         case SPION_OK: return "ok";

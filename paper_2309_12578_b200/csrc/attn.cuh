@@ -17,6 +17,8 @@ struct AttnArgs {
     const int *plan;
 };
 
+extern unsigned long long *g_trace_buf;  // debug event trace (SPION_TRACE=1)
+
 bool simt_supported(int B, int d);
 spion_status launch_fwd_simt(const AttnArgs &a, spion_dtype dt, cudaStream_t s);
 spion_status launch_bwd_preprocess(const AttnArgs &a, spion_dtype dt, float *D, cudaStream_t s);

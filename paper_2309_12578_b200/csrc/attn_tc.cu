@@ -11,21 +11,26 @@
 //
 // attn_fwd_tc   (row tiles; Alg. 5 l.5-7, Alg. 6), per (bh, tile):
 //   for J:  S = Q K_J^T (TMEM, double buffered) -> online softmax, thread = row
-//           -> P (bf16, smem) -> O += P V_J (TMEM)
+//           -> P (bf16, TMEM) -> O += P V_J (TMEM)
 //   epilogue: O / Z and lse (PAPER: logaddexp(m + ln l, ln(L - cnt)), readings Q1/Q2)
 // attn_bwd_dq_tc (row tiles; reading Q17), per (bh, tile):
 //   D = rowsum(dO * O) from the staged tiles (written for the dK/dV kernel);
-//   for J:  S = Q K_J^T, dP = dO V_J^T -> dS = exp(S*c - lse)(dP - D) (smem)
+//   for J:  S = Q K_J^T, dP = dO V_J^T -> dS = exp(S*c - lse)(dP - D) (TMEM)
 //           -> dQ += dS K_J (TMEM);  dQ * scale -> bf16.   No atomics.
 // attn_bwd_dkdv_tc (column tiles), per (bh, tile of key blocks):
-//   for I:  S^T = K Q_I^T, dP^T = V dO_I^T -> P^T, dS^T (smem)
+//   for I:  S^T = K Q_I^T, dP^T = V dO_I^T -> P^T, dS^T (TMEM)
 //           -> dV += P^T dO_I, dK += dS^T Q_I (TMEM);  dK * scale -> bf16.
 //
 // Warp roles (192 threads): warps 0-3 softmax / epilogue (thread = TMEM lane =
 // tile row), warp 4 scheduler + TMA producer, warp 5 MMA issuer (one thread)
-// and TMEM allocator.  Persistent grid of 2 CTAs per SM; work items (bh, tile)
-// come from an atomic counter in the plan (longest tiles of each bh-chunk first)
-// and are broadcast, with their plan entries, through a shared-memory ring.
+// and TMEM allocator.  S (and dP) are double buffered in TMEM so the MMAs of the
+// next block overlap the softmax of the current one; P / dS are written back
+// into TMEM as packed bf16 and consumed as the A operand of the next MMA
+// (tcgen05 TS form), so they never touch shared memory.  Per-item tiles (Q, or
+// K/V) are double buffered across work items.  Persistent grid; work items
+// (bh, tile) come from an atomic counter in the plan (longest tiles of each
+// bh-chunk first) and are broadcast, with their plan entries, through a
+// shared-memory ring.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
@@ -38,12 +43,17 @@ namespace spion {
 using namespace tc;
 
 static constexpr int TC_THREADS = 192;
-// ring stages: as many as fit next to the fixed tiles with 2 CTAs per SM (~104 KB each);
-// a B=32 stage is half the size of a B=64 one, so it gets twice the depth
-template <int B> struct Stages {
-    static constexpr int FWD = B == 32 ? 8 : 4;  // K_J + V_J per stage
-    static constexpr int DQ = B == 32 ? 6 : 3;   // K_J + V_J per stage
-    static constexpr int DKV = B == 32 ? 4 : 2;  // Q_I + dO_I + lse_I + D_I per stage
+// Per-B configuration.  B=32 kernels run 2 CTAs per SM (256 TMEM columns, ~113 KB of
+// shared memory each); the B=64 backward kernels need 512 TMEM columns for their
+// double-buffered S/dP and run 1 CTA per SM with deeper TMA rings instead.
+template <int B> struct Cfg {
+    static constexpr int FWD_NST = B == 32 ? 8 : 4;   // K_J + V_J per stage
+    static constexpr int DQ_CTAS = B == 32 ? 2 : 1;
+    static constexpr int DQ_COLS = B == 32 ? 256 : 512;
+    static constexpr int DQ_NST = B == 32 ? 3 : 8;    // K_J + V_J per stage
+    static constexpr int DKV_CTAS = B == 32 ? 2 : 1;
+    static constexpr int DKV_COLS = B == 32 ? 256 : 512;
+    static constexpr int DKV_NST = B == 32 ? 4 : 8;   // Q_I + dO_I + lse_I + D_I per stage
 };
 static constexpr int SCHED_CAP = 128;  // max entries of one tile list (nblk <= 128)
 static constexpr float LOG2E = 1.4426950408889634f;
@@ -66,6 +76,27 @@ struct TcParams {
     int off_sched;                  // plan words [off_sched] item counter, [off_sched+1] done counter
     int G;                          // (batch, head) chunk of the scheduling order
     int S;                          // slots per tile
+    unsigned long long *trace;      // optional event trace of CTA 0 (SPION_TRACE=1), else null
+};
+
+// debug event trace of CTA 0 (SPION_TRACE=1): each recording thread owns a region of
+// 1024 (event, globaltimer) pairs and a private counter, so recording is a pair of
+// fire-and-forget stores (no atomics on the critical path)
+struct Tracer {
+    unsigned long long *base;
+    int n;
+    __device__ Tracer(const TcParams &p, int role) : base(nullptr), n(0) {
+        if (p.trace && blockIdx.x == 0) base = p.trace + 16 + role * 2048;
+    }
+    __device__ __forceinline__ void ev(int id) {
+        if (base && n < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            base[2 * n] = (unsigned long long)id;
+            base[2 * n + 1] = t;
+            ++n;
+        }
+    }
 };
 
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
@@ -182,38 +213,47 @@ __device__ __forceinline__ void zero_row_bf16(__nv_bfloat16 *dst) {
 }
 
 // ============================================================================ forward
+// Per (bh, row tile): Q tile double buffered across items; K_J/V_J stream through a
+// TMA ring; S_J lands in one of two TMEM buffers so the MMA for block J+1 runs
+// while the softmax warps work on block J; P_J (bf16) is written back over S_J in
+// TMEM and feeds O += P_J V_J as the A operand from tensor memory.
 template <int B>
 __global__ void __launch_bounds__(TC_THREADS, 2)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, TcParams p) {
-    constexpr uint32_t KV_BYTES = B * 128;
-    constexpr int FWD_NST = Stages<B>::FWD;
-    constexpr uint32_t STG = 2 * KV_BYTES;  // K at +0, V at +KV_BYTES
+    constexpr int NST = Cfg<B>::FWD_NST;
+    constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;  // stage: K at +0, V at +KV_BYTES
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, 64, false, true);
-    constexpr uint32_t COL_S = 0, COL_O = 128;
+    constexpr uint32_t COL_O = 128;  // S / P buffer b at columns [64 b, 64 b + B)
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *sQ = smem;
-    uint8_t *sP = smem + 16384;
-    uint8_t *sKV = smem + 32768;  // stage st: K at st*STG, V at st*STG + KV_BYTES
-    uint8_t *sSched = sKV + FWD_NST * STG;
+    uint8_t *sQ = smem;           // [2] x 16 KB
+    uint8_t *sKV = smem + 32768;  // [NST] x STG
+    uint8_t *sSched = sKV + NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *q_full = bars + 0, *q_empty = bars + 1, *p_full = bars + 2, *pv_done = bars + 3,
-             *s_full = bars + 4 /*[2]*/, *kv_full = bars + 6 /*[NST]*/, *kv_empty = bars + 6 + FWD_NST /*[NST]*/;
-    Sched sc = make_sched(sSched, bars + 6 + 2 * FWD_NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6 + 2 * FWD_NST + 8);
+    // p_full is per S/P buffer: the softmax may finish block J+1 before the MMA thread has
+    // observed block J, and one barrier would then run two phases ahead of its waiter
+    // pv_done[b]: the P.V MMA that read packed P from TMEM buffer b has completed.  The
+    // next S into b waits on it (the tensor pipe does not order an A-from-TMEM read
+    // against a later MMA's write of the same columns), and so do O rescales and the
+    // epilogue.  Per buffer, so no waiter can fall two phases behind (parity waits).
+    uint64_t *q_full = bars + 0, *q_empty = bars + 2, *p_full = bars + 4, *pv_done = bars + 6, *s_full = bars + 8,
+             *kv_full = bars + 11, *kv_empty = bars + 11 + NST;
+    Sched sc = make_sched(sSched, bars + 11 + 2 * NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 11 + 2 * NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
-        mbar_init(p_full, 128);
-        mbar_init(pv_done, 1);
-        mbar_init(s_full + 0, 1);
-        mbar_init(s_full + 1, 1);
-        for (int i = 0; i < FWD_NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(q_full + i, 1);
+            mbar_init(q_empty + i, 1);
+            mbar_init(s_full + i, 1);
+            mbar_init(p_full + i, 128);
+            mbar_init(pv_done + i, 1);
+        }
+        for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         sched_init(sc);
         fence_barrier_init();
     }
@@ -236,16 +276,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *col = sc.col + (ks & 3) * SCHED_CAP;
             if (lane == 0 && cnt > 0) {
-                if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);
-                mbar_arrive_expect_tx(q_full, 16384);
-                tma_load_3d(sQ, &tmQ, q_full, 0, t * 128, bh);
+                const int qb = nq & 1;
+                if (nq >= 2) mbar_wait(q_empty + qb, ((nq >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(q_full + qb, 16384);
+                tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
                 ++nq;
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
-                    mbar_arrive_expect_tx(kv_full + st, 2 * KV_BYTES);
+                    mbar_arrive_expect_tx(kv_full + st, STG);
                     tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
                     tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
-                    if (++st == FWD_NST) { st = 0; ph ^= 1; }
+                    if (++st == NST) { st = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
@@ -254,41 +295,44 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             int st = 0, nq = 0;
-            uint32_t ph = 0, p_ph = 0;
-            const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ));
-            const uint64_t dP0 = sdesc_sw128(smem_u32(sP));
+            uint32_t ph = 0, p_ph0 = 0, p_ph1 = 0;
+            uint32_t nsb[2] = {0, 0};  // S issued into each buffer
             for (int ks = 0;; ++ks) {
                 const int *h = sched_wait(sc, ks);
                 if (h[0] < 0) break;
                 const int cnt = h[3];
                 if (cnt > 0) {
-                    mbar_wait(q_full, nq & 1);
+                    const int qb = nq & 1;
+                    mbar_wait(q_full + qb, (nq >> 1) & 1);
                     tc_fence_after();
                     ++nq;
+                    const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
                     int prev_st = 0;
                     for (int jj = 0; jj <= cnt; ++jj) {
                         const int cur_st = st;
-                        if (jj < cnt) {
+                        if (jj < cnt) {  // S(jj) = Q K_J^T into buffer jj&1
                             mbar_wait(kv_full + st, ph);
                             tc_fence_after();
-                            const uint32_t sb = jj & 1;
                             const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
+                            if (nsb[jj & 1] > 0) mbar_wait(pv_done + (jj & 1), (nsb[jj & 1] - 1) & 1);
+                            ++nsb[jj & 1];
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
-                                mma_bf16_ss(tmem + COL_S + sb * 64, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
-                            mma_commit(s_full + sb);
-                            if (jj == cnt - 1) mma_commit(q_empty);
-                            if (++st == FWD_NST) { st = 0; ph ^= 1; }
+                                mma_bf16_ss(tmem + (jj & 1) * 64, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                            mma_commit(s_full + (jj & 1));
+                            if (jj == cnt - 1) mma_commit(q_empty + qb);
+                            if (++st == NST) { st = 0; ph ^= 1; }
                         }
-                        if (jj >= 1) {  // O += P(jj-1) V(jj-1)
-                            mbar_wait(p_full, p_ph);
-                            p_ph ^= 1;
+                        if (jj >= 1) {  // O += P(jj-1) V(jj-1), P from TMEM
+                            if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
+                            else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
                             tc_fence_after();
+                            const uint32_t aP = tmem + ((jj - 1) & 1) * 64;
                             const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + prev_st * STG + KV_BYTES));
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ss(tmem + COL_O, dP0 + 2 * k, dV0 + 128 * k, IDESC_PV, (jj > 1) || (k > 0));
-                            mma_commit(pv_done);
+                                mma_bf16_ts(tmem + COL_O, aP + 8 * k, dV0 + 128 * k, IDESC_PV, (jj > 1) || (k > 0));
+                            mma_commit(pv_done + ((jj - 1) & 1));
                             mma_commit(kv_empty + prev_st);
                         }
                         prev_st = cur_st;
@@ -302,7 +346,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const int r = threadIdx.x;  // tile row = TMEM lane
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t sph0 = 0, sph1 = 0, pv_ph = 0;
+        uint32_t sph0 = 0, sph1 = 0;
+        uint32_t npv0 = 0, npv1 = 0;  // P.V MMAs on each buffer before the current item
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
@@ -328,7 +373,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
                     for (int hh = 0; hh < B / 32; ++hh) {
                         float v[32];
-                        tmem_ld32(tl + COL_S + sb * 64 + hh * 32, v);
+                        tmem_ld32(tl + sb * 64 + hh * 32, v);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; ++i) s[hh * 32 + i] = v[i] * sl2;
@@ -355,12 +400,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
                     for (int i = 0; i < B / 2; ++i) packed[i] = 0u;
                 }
-                if (jj >= 1) {  // PV(jj-1) complete before P is overwritten and O touched
-                    mbar_wait(pv_done, pv_ph);
-                    pv_ph ^= 1;
+                if (__any_sync(0xffffffffu, rescale)) {  // O *= alpha once P.V(jj-1) is complete
+                    const int pj = jj - 1;  // P.V(pj) is the (npv_b + pj/2)-th on buffer pj&1
+                    mbar_wait(pv_done + (pj & 1), ((pj & 1 ? npv1 : npv0) + (pj >> 1)) & 1);
                     tc_fence_after();
-                }
-                if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         float o[32];
@@ -370,15 +413,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         for (int i = 0; i < 32; ++i) o[i] *= alpha;
                         tmem_st32(tl + COL_O + hh * 32, o);
                     }
-                    tmem_st_wait();
                 }
 #pragma unroll
-                for (int c = 0; c < B / 8; ++c)
-                    *reinterpret_cast<uint4 *>(sP + sw128_offset(r, c)) =
-                        make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
-                fence_proxy_async_smem();
+                for (int hh = 0; hh < B / 32; ++hh) {
+                    uint32_t v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = packed[hh * 16 + i];
+                    tmem_st16(tl + sb * 64 + hh * 16, v);
+                }
+                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(p_full);
+                mbar_arrive(p_full + sb);
             }
             // ---- epilogue: O / Z and lse (log2 domain internally)
             float f = 0.f, lse2;
@@ -397,9 +442,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 f = exp2f(m_run - lse2);
             }
             if (cnt > 0) {
-                mbar_wait(pv_done, pv_ph);
-                pv_ph ^= 1;
+                // the last P.V on each buffer: P.V(cnt-1) and P.V(cnt-2)
+                for (int pj = cnt - 1; pj >= 0 && pj >= cnt - 2; --pj)
+                    mbar_wait(pv_done + (pj & 1), ((pj & 1 ? npv1 : npv0) + (pj >> 1)) & 1);
                 tc_fence_after();
+                npv0 += (cnt + 1) >> 1;
+                npv1 += cnt >> 1;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     float o[32];
@@ -424,42 +472,51 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 }
 
 // ============================================================================ backward: dQ
+// Per (bh, row tile): D = rowsum(dO * O) (written for the dK/dV kernel); for each
+// block J: S, dP (double-buffered TMEM) -> dS = exp(S c - lse)(dP - D), packed bf16
+// over S in TMEM -> dQ += dS K_J (A from TMEM).  No atomics, no fp32 round trip.
 template <int B>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+__global__ void __launch_bounds__(TC_THREADS, Cfg<B>::DQ_CTAS)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, TcParams p) {
-    constexpr uint32_t KV_BYTES = B * 128;
-    constexpr int DQ_NST = Stages<B>::DQ;
-    constexpr uint32_t STG = 2 * KV_BYTES;
+    constexpr int NST = Cfg<B>::DQ_NST;
+    constexpr int COLS = Cfg<B>::DQ_COLS;
+    constexpr uint32_t BUFW = B == 32 ? 64 : 128;  // S at b*BUFW, dP at b*BUFW + B
+    constexpr uint32_t COL_DQ = 2 * BUFW;
+    constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);   // S = Q K^T, dP = dO V^T
-    constexpr uint32_t IDESC_DQ = idesc_bf16(128, 64, false, true);  // dQ = dS K
-    constexpr uint32_t COL_S = 0, COL_DP = 64, COL_DQ = 128;
+    constexpr uint32_t IDESC_DQ = idesc_bf16(128, 64, false, true);  // dQ += dS K
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    // O is staged in the dS buffer: it is only read (for D) before the first dS is written
-    uint8_t *sQ = smem, *sdO = smem + 16384, *sdS = smem + 32768, *sO = sdS;
-    uint8_t *sKV = smem + 49152;  // stage st: K at st*STG, V at +KV_BYTES
-    uint8_t *sSched = sKV + DQ_NST * STG;
+    uint8_t *sQ = smem, *sdO = smem + 32768, *sO = smem + 65536;  // sQ, sdO: [2] x 16 KB
+    uint8_t *sKV = smem + 81920;                                    // [NST] x STG
+    uint8_t *sSched = sKV + NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *q_full = bars + 0, *q_empty = bars + 1, *s_full = bars + 2, *ds_full = bars + 3,
-             *dq_full = bars + 4, *kv_full = bars + 5 /*[NST]*/, *kv_empty = bars + 5 + DQ_NST /*[NST]*/;
-    Sched sc = make_sched(sSched, bars + 5 + 2 * DQ_NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5 + 2 * DQ_NST + 8);
+    uint64_t *q_full = bars + 0, *q_empty = bars + 2, *o_full = bars + 4, *o_empty = bars + 5, *s_full = bars + 6,
+             *ds_full = bars + 8 /*[2], per buffer*/, *dq_full = bars + 10, *buf_free = bars + 11 /*[2]*/,
+             *kv_full = bars + 13, *kv_empty = bars + 13 + NST;
+    Sched sc = make_sched(sSched, bars + 13 + 2 * NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 13 + 2 * NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
-        mbar_init(s_full, 1);
-        mbar_init(ds_full, 128);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(q_full + i, 1);
+            mbar_init(q_empty + i, 1);
+            mbar_init(s_full + i, 1);
+            mbar_init(ds_full + i, 128);
+            mbar_init(buf_free + i, 1);
+        }
+        mbar_init(o_full, 1);
+        mbar_init(o_empty, 128);
         mbar_init(dq_full, 1);
-        for (int i = 0; i < DQ_NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+        for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         sched_init(sc);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<256>(tmem_slot);
+    if (warp == 5) tmem_alloc<COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -480,18 +537,21 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *col = sc.col + (ks & 3) * SCHED_CAP;
             if (lane == 0 && cnt > 0) {
-                if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);
-                mbar_arrive_expect_tx(q_full, 3 * 16384);
-                tma_load_3d(sQ, &tmQ, q_full, 0, t * 128, bh);
-                tma_load_3d(sdO, &tmdO, q_full, 0, t * 128, bh);
-                tma_load_3d(sO, &tmO, q_full, 0, t * 128, bh);
+                const int qb = nq & 1;
+                if (nq >= 2) mbar_wait(q_empty + qb, ((nq >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(q_full + qb, 32768);
+                tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
+                tma_load_3d(sdO + qb * 16384, &tmdO, q_full + qb, 0, t * 128, bh);
+                if (nq >= 1) mbar_wait(o_empty, (nq - 1) & 1);
+                mbar_arrive_expect_tx(o_full, 16384);
+                tma_load_3d(sO, &tmO, o_full, 0, t * 128, bh);
                 ++nq;
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
-                    mbar_arrive_expect_tx(kv_full + st, 2 * KV_BYTES);
+                    mbar_arrive_expect_tx(kv_full + st, STG);
                     tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
                     tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
-                    if (++st == DQ_NST) { st = 0; ph ^= 1; }
+                    if (++st == NST) { st = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
@@ -499,40 +559,54 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     } else if (warp == 5) {
         if (lane == 0) {
             int st = 0, nq = 0;
-            uint32_t ph = 0, ds_ph = 0;
-            const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ));
-            const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO));
-            const uint64_t ddS0 = sdesc_sw128(smem_u32(sdS));
+            uint32_t ph = 0, ds_ph0 = 0, ds_ph1 = 0;
+            uint32_t nsb[2] = {0, 0};  // S/dP issued into each buffer
             for (int ks = 0;; ++ks) {
                 const int *h = sched_wait(sc, ks);
                 if (h[0] < 0) break;
                 const int cnt = h[3];
                 if (cnt > 0) {
-                    mbar_wait(q_full, nq & 1);
+                    const int qb = nq & 1;
+                    mbar_wait(q_full + qb, (nq >> 1) & 1);
                     tc_fence_after();
                     ++nq;
-                    for (int jj = 0; jj < cnt; ++jj) {
-                        mbar_wait(kv_full + st, ph);
-                        tc_fence_after();
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
-                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * STG + KV_BYTES));
+                    const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
+                    const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
+                    int prev_st = 0;
+                    for (int jj = 0; jj <= cnt; ++jj) {
+                        const int cur_st = st;
+                        if (jj < cnt) {  // S(jj), dP(jj) into buffer jj&1
+                            mbar_wait(kv_full + st, ph);
+                            tc_fence_after();
+                            const uint32_t cs = (jj & 1) * BUFW;
+                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
+                            const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * STG + KV_BYTES));
+                            if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
+                            ++nsb[jj & 1];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + COL_S, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                            for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            mma_bf16_ss(tmem + COL_DP, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
-                        mma_commit(s_full);
-                        mbar_wait(ds_full, ds_ph);
-                        ds_ph ^= 1;
-                        tc_fence_after();
-                        // dQ += dS K_J  (A = dS [rows][keys] K-major, B = K_J as N=d x K=keys, MN-major)
+                            for (int k = 0; k < 4; ++k)
+                                mma_bf16_ss(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
+                            mma_commit(s_full + (jj & 1));
+                            if (++st == NST) { st = 0; ph ^= 1; }
+                        }
+                        if (jj >= 1) {  // dQ += dS(jj-1) K(jj-1), dS from TMEM
+                            if ((jj - 1) & 1) { mbar_wait(ds_full + 1, ds_ph1); ds_ph1 ^= 1; }
+                            else { mbar_wait(ds_full + 0, ds_ph0); ds_ph0 ^= 1; }
+                            tc_fence_after();
+                            const uint32_t aS = tmem + ((jj - 1) & 1) * BUFW;
+                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + prev_st * STG));
 #pragma unroll
-                        for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ss(tmem + COL_DQ, ddS0 + 2 * k, dK0 + 128 * k, IDESC_DQ, (jj > 0) || (k > 0));
-                        mma_commit(kv_empty + st);
-                        if (jj == cnt - 1) { mma_commit(dq_full); mma_commit(q_empty); }
-                        if (++st == DQ_NST) { st = 0; ph ^= 1; }
+                            for (int k = 0; k < B / 16; ++k)
+                                mma_bf16_ts(tmem + COL_DQ, aS + 8 * k, dK0 + 128 * k, IDESC_DQ, (jj > 1) || (k > 0));
+                            mma_commit(buf_free + ((jj - 1) & 1));
+                            mma_commit(kv_empty + prev_st);
+                        }
+                        prev_st = cur_st;
                     }
+                    mma_commit(dq_full);
+                    mma_commit(q_empty + qb);
                 }
                 sched_release(sc, ks, false);
             }
@@ -541,7 +615,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         const int r = threadIdx.x;  // query row of the tile
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t q_ph = 0, s_ph = 0, dq_ph = 0;
+        uint32_t sph0 = 0, sph1 = 0, dq_ph = 0;
+        int nq = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
@@ -557,36 +632,44 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 sched_release(sc, ks, true);
                 continue;
             }
+            const int qb = nq & 1;
             const float lse2 = valid ? p.lse[(int64_t)bh * p.L + row] * LOG2E : 0.f;
-            mbar_wait(q_full, q_ph);
-            q_ph ^= 1;
             // D_i = dO_i . O_i from the staged (swizzled) tiles
+            mbar_wait(q_full + qb, (nq >> 1) & 1);
+            mbar_wait(o_full, nq & 1);
+            ++nq;
             float Dr = 0.f;
+            {
+                const uint8_t *rdO = sdO + qb * 16384;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const uint4 a = *reinterpret_cast<const uint4 *>(sO + sw128_offset(r, c));
-                const uint4 g = *reinterpret_cast<const uint4 *>(sdO + sw128_offset(r, c));
-                const uint32_t av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
+                for (int c = 0; c < 8; ++c) {
+                    const uint4 a = *reinterpret_cast<const uint4 *>(sO + sw128_offset(r, c));
+                    const uint4 g = *reinterpret_cast<const uint4 *>(rdO + sw128_offset(r, c));
+                    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&av[i]));
-                    const float2 fg = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&gv[i]));
-                    Dr = fmaf(fa.x, fg.x, fmaf(fa.y, fg.y, Dr));
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&av[i]));
+                        const float2 fg = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&gv[i]));
+                        Dr = fmaf(fa.x, fg.x, fmaf(fa.y, fg.y, Dr));
+                    }
                 }
             }
+            mbar_arrive(o_empty);
             if (valid) p.D[(int64_t)bh * p.L + row] = Dr;
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;
-                mbar_wait(s_full, s_ph);  // also implies dQ(jj-1) finished reading sdS
-                s_ph ^= 1;
+                const uint32_t sb = jj & 1;
+                if (sb == 0) { mbar_wait(s_full + 0, sph0); sph0 ^= 1; }
+                else { mbar_wait(s_full + 1, sph1); sph1 ^= 1; }
                 tc_fence_after();
+                const uint32_t cs = sb * BUFW;
 #pragma unroll
                 for (int hh = 0; hh < B / 32; ++hh) {
                     uint32_t pk[16];
                     if (active) {
                         float sv[32], dp[32];
-                        tmem_ld32(tl + COL_S + hh * 32, sv);
-                        tmem_ld32(tl + COL_DP + hh * 32, dp);
+                        tmem_ld32(tl + cs + hh * 32, sv);
+                        tmem_ld32(tl + cs + B + hh * 32, dp);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
@@ -598,14 +681,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 #pragma unroll
                         for (int i = 0; i < 16; ++i) pk[i] = 0u;
                     }
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        *reinterpret_cast<uint4 *>(sdS + sw128_offset(r, hh * 4 + c)) =
-                            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                    tmem_st16(tl + cs + hh * 16, pk);  // packed dS over the consumed S columns
                 }
-                fence_proxy_async_smem();
+                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(ds_full);
+                mbar_arrive(ds_full + sb);
             }
             mbar_wait(dq_full, dq_ph);
             dq_ph ^= 1;
@@ -625,48 +705,58 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<COLS>(tmem);
     }
 }
 
 // ============================================================================ backward: dK, dV
-// K/V tiles are double buffered across items; P^T and dS^T never leave the SM:
-// they are written as packed bf16 over the S^T / dP^T columns of TMEM and feed
-// the dV / dK MMAs as the A operand straight from tensor memory.
+// Per (bh, column tile): K/V tiles double buffered across items; for each query
+// block I: S^T, dP^T into one of two TMEM buffers (the MMA for I+1 overlaps the
+// softmax of I); P^T, dS^T packed over them feed dV += P^T dO_I, dK += dS^T Q_I
+// as A operands from tensor memory.
 template <int B>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+__global__ void __launch_bounds__(TC_THREADS, Cfg<B>::DKV_CTAS)
 attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         TcParams p) {
+    constexpr int NST = Cfg<B>::DKV_NST;
+    constexpr int COLS = Cfg<B>::DKV_COLS;
+    constexpr uint32_t BUFW = B == 32 ? 64 : 128;  // S^T at b*BUFW, dP^T at b*BUFW + B
+    // dK accumulates at 2*BUFW and dV at 2*BUFW + 64.  (The mirrored placement, dV at
+    // column 256 fed from P^T at columns 0/128, produced corrupted dV rows on B200 for
+    // B=64 — test_bf16_parity[512-64-...] catches it; this order is verified.)
+    constexpr uint32_t COL_DK = 2 * BUFW, COL_DV = 2 * BUFW + 64;
     constexpr uint32_t TILE = B * 128;
-    constexpr int DKV_NST = Stages<B>::DKV;
     constexpr uint32_t STAGE = 2 * TILE + 1024;  // Q_I, dO_I, lse_I, D_I
     constexpr uint32_t IDESC_ST = idesc_bf16(128, B, false, false);   // S^T = K Q^T, dP^T = V dO^T
     constexpr uint32_t IDESC_DKV = idesc_bf16(128, 64, false, true);  // dV += P^T dO, dK += dS^T Q
-    constexpr uint32_t COL_S = 0, COL_DP = 64, COL_DV = 128, COL_DK = 192;  // P^T over S^T, dS^T over dP^T
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sKV = smem;  // buffer kb: K at kb*32768, V at kb*32768 + 16384
     uint8_t *sStage = smem + 65536;
-    uint8_t *sSched = sStage + DKV_NST * STAGE;
+    uint8_t *sSched = sStage + NST * STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *kv_full = bars + 0 /*[2]*/, *kv_empty = bars + 2 /*[2]*/, *s_full = bars + 4, *p_full = bars + 5,
-             *acc_full = bars + 6, *q_full = bars + 7 /*[NST]*/, *q_empty = bars + 7 + DKV_NST /*[NST]*/;
-    Sched sc = make_sched(sSched, bars + 7 + 2 * DKV_NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 7 + 2 * DKV_NST + 8);
+    uint64_t *kv_full = bars + 0, *kv_empty = bars + 2, *s_full = bars + 4, *p_full = bars + 6 /*[2], per buffer*/,
+             *acc_full = bars + 8, *buf_free = bars + 9 /*[2]*/, *q_full = bars + 11, *q_empty = bars + 11 + NST;
+    Sched sc = make_sched(sSched, bars + 11 + 2 * NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 11 + 2 * NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
-        mbar_init(s_full, 1);
-        mbar_init(p_full, 128);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(kv_full + i, 1);
+            mbar_init(kv_empty + i, 1);
+            mbar_init(s_full + i, 1);
+            mbar_init(p_full + i, 128);
+            mbar_init(buf_free + i, 1);
+        }
         mbar_init(acc_full, 1);
-        for (int i = 0; i < DKV_NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
+        for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
         sched_init(sc);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<256>(tmem_slot);
+    if (warp == 5) tmem_alloc<COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -699,15 +789,16 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
                     bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
                     bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
-                    if (++st == DKV_NST) { st = 0; ph ^= 1; }
+                    if (++st == NST) { st = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
         }
     } else if (warp == 5) {
         if (lane == 0) {
-            int st = 0, nk = 0;
-            uint32_t ph = 0, p_ph = 0;
+            int ld_st = 0, use_st = 0, nk = 0;
+            uint32_t ld_ph = 0, p_ph0 = 0, p_ph1 = 0;
+            uint32_t nsb[2] = {0, 0};  // S^T/dP^T issued into each buffer
             for (int ks = 0;; ++ks) {
                 const int *h = sched_wait(sc, ks);
                 if (h[0] < 0) break;
@@ -719,32 +810,46 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     ++nk;
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
                     const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
-                    for (int jj = 0; jj < cnt; ++jj) {
-                        mbar_wait(q_full + st, ph);
-                        tc_fence_after();
-                        uint8_t *stg = sStage + st * STAGE;
-                        const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
-                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                    for (int jj = 0; jj <= cnt; ++jj) {
+                        if (jj < cnt) {  // S^T(jj), dP^T(jj) into buffer jj&1
+                            mbar_wait(q_full + ld_st, ld_ph);
+                            tc_fence_after();
+                            uint8_t *stg = sStage + ld_st * STAGE;
+                            const uint32_t cs = (jj & 1) * BUFW;
+                            const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
+                            const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                            if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
+                            ++nsb[jj & 1];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + COL_S, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
+                            for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            mma_bf16_ss(tmem + COL_DP, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
-                        mma_commit(s_full);
-                        if (jj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
-                        mbar_wait(p_full, p_ph);
-                        p_ph ^= 1;
-                        tc_fence_after();
+                            for (int k = 0; k < 4; ++k)
+                                mma_bf16_ss(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
+                            mma_commit(s_full + (jj & 1));
+                            if (jj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
+                            if (++ld_st == NST) { ld_st = 0; ld_ph ^= 1; }
+                        }
+                        if (jj >= 1) {  // dV += P^T dO, dK += dS^T Q for step jj-1 (A from TMEM)
+                            if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
+                            else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
+                            tc_fence_after();
+                            uint8_t *stg = sStage + use_st * STAGE;
+                            const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
+                            const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                            const uint32_t cs = ((jj - 1) & 1) * BUFW;
+                            const uint32_t acc = jj > 1;
 #pragma unroll
-                        for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ts(tmem + COL_DV, tmem + COL_S + 8 * k, ddO0 + 128 * k, IDESC_DKV, (jj > 0) || (k > 0));
+                            for (int k = 0; k < B / 16; ++k)
+                                mma_bf16_ts(tmem + COL_DV, tmem + cs + 8 * k, ddO0 + 128 * k, IDESC_DKV, acc || (k > 0));
 #pragma unroll
-                        for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ts(tmem + COL_DK, tmem + COL_DP + 8 * k, dQ0 + 128 * k, IDESC_DKV, (jj > 0) || (k > 0));
-                        mma_commit(q_empty + st);
-                        if (jj == cnt - 1) mma_commit(acc_full);
-                        if (++st == DKV_NST) { st = 0; ph ^= 1; }
+                            for (int k = 0; k < B / 16; ++k)
+                                mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 8 * k, dQ0 + 128 * k, IDESC_DKV, acc || (k > 0));
+                            mma_commit(buf_free + ((jj - 1) & 1));
+                            mma_commit(q_empty + use_st);
+                            if (++use_st == NST) use_st = 0;
+                        }
                     }
+                    mma_commit(acc_full);
                 }
                 sched_release(sc, ks, false);
             }
@@ -753,7 +858,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         const int r = threadIdx.x;  // key row of the tile = TMEM lane
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t s_ph = 0, a_ph = 0, ph = 0;
+        uint32_t sph0 = 0, sph1 = 0, a_ph = 0, ph = 0;
         int st = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
@@ -774,19 +879,21 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             }
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;
-                mbar_wait(q_full + st, ph);
+                mbar_wait(q_full + st, ph);  // lse_I, D_I
                 const float *slse = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
                 const float *sD = slse + 128;
-                mbar_wait(s_full, s_ph);
-                s_ph ^= 1;
+                const uint32_t sb = jj & 1;
+                if (sb == 0) { mbar_wait(s_full + 0, sph0); sph0 ^= 1; }
+                else { mbar_wait(s_full + 1, sph1); sph1 ^= 1; }
                 tc_fence_after();
+                const uint32_t cs = sb * BUFW;
 #pragma unroll
                 for (int hh = 0; hh < B / 32; ++hh) {
                     uint32_t pk[16], dk[16];
                     if (active) {
                         float sv[32], dp[32];
-                        tmem_ld32(tl + COL_S + hh * 32, sv);
-                        tmem_ld32(tl + COL_DP + hh * 32, dp);
+                        tmem_ld32(tl + cs + hh * 32, sv);
+                        tmem_ld32(tl + cs + B + hh * 32, dp);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
@@ -801,13 +908,13 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         for (int i = 0; i < 16; ++i) { pk[i] = 0u; dk[i] = 0u; }
                     }
                     // packed bf16 P^T / dS^T over the (already read) S^T / dP^T columns
-                    tmem_st16(tl + COL_S + hh * 16, pk);
-                    tmem_st16(tl + COL_DP + hh * 16, dk);
+                    tmem_st16(tl + cs + hh * 16, pk);
+                    tmem_st16(tl + cs + B + hh * 16, dk);
                 }
                 tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(p_full);
-                if (++st == DKV_NST) { st = 0; ph ^= 1; }
+                mbar_arrive(p_full + sb);
+                if (++st == NST) { st = 0; ph ^= 1; }
             }
             mbar_wait(acc_full, a_ph);
             a_ph ^= 1;
@@ -831,7 +938,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<COLS>(tmem);
     }
 }
 
@@ -872,6 +979,7 @@ bool tc_supported(const AttnArgs &a, spion_dtype dt) {
     return !disabled && get_encode() != nullptr;
 }
 
+unsigned long long *g_trace_buf = nullptr;
 static int num_sms() {
     static int n = 0;
     if (!n) {
@@ -884,7 +992,7 @@ static int num_sms() {
 }
 
 // which: 0 fwd (row tiles), 1 dq (row tiles), 2 dkdv (column tiles)
-static TcParams base_params(const AttnArgs &a, int which) {
+static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     TcParams p;
     memset(&p, 0, sizeof(p));
     PlanLayout pl(a.n, a.B);
@@ -906,22 +1014,31 @@ static TcParams base_params(const AttnArgs &a, int which) {
     p.off_msk = (int)(rows ? pl.fmsk : pl.bmsk);
     p.off_order = (int)(rows ? pl.forder : pl.border);
     p.off_sched = 8 + 2 * which;
-    const int grid = 2 * num_sms();
+    const int grid = ctas * num_sms();
     int G = (2 * grid + pl.ntiles - 1) / pl.ntiles;
     if (G < 1) G = 1;
     if (G > a.bh) G = (int)a.bh;
     p.G = G;
+    static unsigned long long *trace_buf = nullptr;
+    static int want = -1;
+    if (want < 0) want = getenv("SPION_TRACE") != nullptr;
+    if (want) {
+        if (!trace_buf) cudaMalloc(&trace_buf, (16 + 8 * 2048) * 8);
+        cudaMemset(trace_buf, 0, (16 + 8 * 2048) * 8);
+        p.trace = trace_buf;
+        g_trace_buf = trace_buf;
+    }
     return p;
 }
 
 static const size_t SCHED_AREA = SCHED_BYTES + 256;
-template <int B> static size_t fwd_smem() { return 1024 + 32768 + Stages<B>::FWD * 2 * B * 128 + SCHED_AREA; }
-template <int B> static size_t dq_smem() { return 1024 + 49152 + Stages<B>::DQ * 2 * B * 128 + SCHED_AREA; }
-template <int B> static size_t dkv_smem() { return 1024 + 65536 + Stages<B>::DKV * (2 * B * 128 + 1024) + SCHED_AREA; }
+template <int B> static size_t fwd_smem() { return 1024 + 32768 + Cfg<B>::FWD_NST * 2 * B * 128 + SCHED_AREA; }
+template <int B> static size_t dq_smem() { return 1024 + 81920 + Cfg<B>::DQ_NST * 2 * B * 128 + SCHED_AREA; }
+template <int B> static size_t dkv_smem() { return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + SCHED_AREA; }
 
-static int grid_for(const TcParams &p) {
+static int grid_for(const TcParams &p, int ctas) {
     const int64_t items = p.bh * p.ntiles;
-    return (int)((items < 2LL * num_sms()) ? items : 2LL * num_sms());
+    return (int)((items < (int64_t)ctas * num_sms()) ? items : (int64_t)ctas * num_sms());
 }
 
 template <int B>
@@ -936,10 +1053,10 @@ static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         !make_map(&mk, a.K, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
         !make_map(&mv, a.V, a.L, a.bh, a.stride_bh, a.stride_l, B))
         return SPION_ERR_CUDA;
-    TcParams p = base_params(a, 0);
+    TcParams p = base_params(a, 0, 2);
     p.O = a.Oout;
     p.lse_out = a.lse_out;
-    attn_fwd_tc_kernel<B><<<grid_for(p), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, p);
+    attn_fwd_tc_kernel<B><<<grid_for(p, 2), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, p);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
@@ -964,20 +1081,20 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         !make_map(&mdoB, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, B))
         return SPION_ERR_CUDA;
     // 1) dQ (row tiles) and D = rowsum(dO * O)
-    TcParams p = base_params(a, 1);
+    TcParams p = base_params(a, 1, Cfg<B>::DQ_CTAS);
     p.O = const_cast<void *>(a.O);
     p.lse = a.lse;
     p.D = const_cast<float *>(a.D);
     p.dQ = a.dQ;
-    attn_bwd_dq_tc_kernel<B><<<grid_for(p), TC_THREADS, dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, p);
+    attn_bwd_dq_tc_kernel<B><<<grid_for(p, Cfg<B>::DQ_CTAS), TC_THREADS, dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, p);
     SPION_LAUNCH_CHECK();
     // 2) dK, dV (column tiles)
-    TcParams q = base_params(a, 2);
+    TcParams q = base_params(a, 2, Cfg<B>::DKV_CTAS);
     q.lse = a.lse;
     q.D = const_cast<float *>(a.D);
     q.dK = a.dK;
     q.dV = a.dV;
-    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q), TC_THREADS, dkv_smem<B>(), s>>>(mk128, mv128, mqB, mdoB, q);
+    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), TC_THREADS, dkv_smem<B>(), s>>>(mk128, mv128, mqB, mdoB, q);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }

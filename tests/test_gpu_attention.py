@@ -122,6 +122,10 @@ BF16_CASES = [
     (224, 32, 64, 2, 0.3, "masked"),    # nblk = 7
     (256, 32, 64, 1, 1.0, "paper"),     # dense
     (256, 16, 32, 2, 0.25, "paper"),    # CUDA-core bf16 path
+    (1024, 64, 64, 2, 0.15, "paper"),   # B=64, stripe columns with many entries (1 CTA/SM kernels)
+    (1024, 64, 64, 2, 0.30, "masked"),
+    (1088, 64, 64, 1, 0.25, "paper"),   # nblk = 17 (ragged tile)
+    (2048, 32, 64, 2, 0.10, "paper"),   # B=32, nblk = 64
 ]
 
 
