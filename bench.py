@@ -207,6 +207,7 @@ def main():
 
     from paper_2309_12578_b200 import spion
     from paper_2309_12578_b200 import _native as N
+    from paper_2309_12578_b200.dist import broadcast_pattern
 
     dist, rank, world, local = dist_setup(args.gpus)
     dev = torch.device(f"cuda:{local}")
@@ -241,7 +242,7 @@ def main():
         if rank == 0 or world == 1:
             spion.pattern(A, B, filter=FILTER, alpha=args.alpha, out=bp)
         if world > 1:
-            dist.broadcast(bp.flat, src=0)     # the per-layer pattern, NCCL over NVLink
+            broadcast_pattern(bp.flat, src=0)  # the per-layer pattern: one NCCL collective
         if ev is not None:
             ev[1].record()
         spion.attn_fwd(q, k, v, bp, args.mode, scale, out=o["o"], lse=o["lse"])
