@@ -275,71 +275,82 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *col = sc.col + (ks & 3) * SCHED_CAP;
-            if (lane == 0 && cnt > 0) {
+            if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the TMA
                 const int qb = nq & 1;
                 if (nq >= 2) mbar_wait(q_empty + qb, ((nq >> 1) - 1) & 1);
-                mbar_arrive_expect_tx(q_full + qb, 16384);
-                tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(q_full + qb, 16384);
+                    tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
+                }
+                __syncwarp();
                 ++nq;
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
-                    mbar_arrive_expect_tx(kv_full + st, STG);
-                    tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                    tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(kv_full + st, STG);
+                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    }
+                    __syncwarp();
                     if (++st == NST) { st = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
         }
     } else if (warp == 5) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            int st = 0, nq = 0;
-            uint32_t ph = 0, p_ph0 = 0, p_ph1 = 0;
-            uint32_t nsb[2] = {0, 0};  // S issued into each buffer
-            for (int ks = 0;; ++ks) {
-                const int *h = sched_wait(sc, ks);
-                if (h[0] < 0) break;
-                const int cnt = h[3];
-                if (cnt > 0) {
-                    const int qb = nq & 1;
-                    mbar_wait(q_full + qb, (nq >> 1) & 1);
-                    tc_fence_after();
-                    ++nq;
-                    const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
-                    int prev_st = 0;
-                    for (int jj = 0; jj <= cnt; ++jj) {
-                        const int cur_st = st;
-                        if (jj < cnt) {  // S(jj) = Q K_J^T into buffer jj&1
-                            mbar_wait(kv_full + st, ph);
-                            tc_fence_after();
-                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
-                            if (nsb[jj & 1] > 0) mbar_wait(pv_done + (jj & 1), (nsb[jj & 1] - 1) & 1);
-                            ++nsb[jj & 1];
+        // ------------------------------------------------------------ MMA issuer (converged warp,
+        // one elected lane issues the tcgen05 instructions)
+        int st = 0, nq = 0;
+        uint32_t ph = 0, p_ph0 = 0, p_ph1 = 0;
+        uint32_t nsb[2] = {0, 0};  // S issued into each buffer
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int cnt = h[3];
+            if (cnt > 0) {
+                const int qb = nq & 1;
+                mbar_wait(q_full + qb, (nq >> 1) & 1);
+                tc_fence_after();
+                ++nq;
+                const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
+                int prev_st = 0;
+                for (int jj = 0; jj <= cnt; ++jj) {
+                    const int cur_st = st;
+                    if (jj < cnt) {  // S(jj) = Q K_J^T into buffer jj&1
+                        mbar_wait(kv_full + st, ph);
+                        if (nsb[jj & 1] > 0) mbar_wait(pv_done + (jj & 1), (nsb[jj & 1] - 1) & 1);
+                        ++nsb[jj & 1];
+                        tc_fence_after();
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
+                        if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_bf16_ss(tmem + (jj & 1) * 64, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
                             mma_commit(s_full + (jj & 1));
                             if (jj == cnt - 1) mma_commit(q_empty + qb);
-                            if (++st == NST) { st = 0; ph ^= 1; }
                         }
-                        if (jj >= 1) {  // O += P(jj-1) V(jj-1), P from TMEM
-                            if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
-                            else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
-                            tc_fence_after();
-                            const uint32_t aP = tmem + ((jj - 1) & 1) * 64;
-                            const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + prev_st * STG + KV_BYTES));
+                        __syncwarp();
+                        if (++st == NST) { st = 0; ph ^= 1; }
+                    }
+                    if (jj >= 1) {  // O += P(jj-1) V(jj-1), P from TMEM
+                        if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
+                        else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
+                        tc_fence_after();
+                        const uint32_t aP = tmem + ((jj - 1) & 1) * 64;
+                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + prev_st * STG + KV_BYTES));
+                        if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
                                 mma_bf16_ts(tmem + COL_O, aP + 8 * k, dV0 + 128 * k, IDESC_PV, (jj > 1) || (k > 0));
                             mma_commit(pv_done + ((jj - 1) & 1));
                             mma_commit(kv_empty + prev_st);
                         }
-                        prev_st = cur_st;
+                        __syncwarp();
                     }
+                    prev_st = cur_st;
                 }
-                sched_release(sc, ks, false);
             }
+            sched_release(sc, ks, true);
         }
     } else {
         // ------------------------------------------------------------ softmax / epilogue
@@ -536,80 +547,93 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *col = sc.col + (ks & 3) * SCHED_CAP;
-            if (lane == 0 && cnt > 0) {
+            if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the TMA
                 const int qb = nq & 1;
                 if (nq >= 2) mbar_wait(q_empty + qb, ((nq >> 1) - 1) & 1);
-                mbar_arrive_expect_tx(q_full + qb, 32768);
-                tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
-                tma_load_3d(sdO + qb * 16384, &tmdO, q_full + qb, 0, t * 128, bh);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(q_full + qb, 32768);
+                    tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
+                    tma_load_3d(sdO + qb * 16384, &tmdO, q_full + qb, 0, t * 128, bh);
+                }
+                __syncwarp();
                 if (nq >= 1) mbar_wait(o_empty, (nq - 1) & 1);
-                mbar_arrive_expect_tx(o_full, 16384);
-                tma_load_3d(sO, &tmO, o_full, 0, t * 128, bh);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(o_full, 16384);
+                    tma_load_3d(sO, &tmO, o_full, 0, t * 128, bh);
+                }
+                __syncwarp();
                 ++nq;
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
-                    mbar_arrive_expect_tx(kv_full + st, STG);
-                    tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                    tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(kv_full + st, STG);
+                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    }
+                    __syncwarp();
                     if (++st == NST) { st = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
         }
     } else if (warp == 5) {
-        if (lane == 0) {
-            int st = 0, nq = 0;
-            uint32_t ph = 0, ds_ph0 = 0, ds_ph1 = 0;
-            uint32_t nsb[2] = {0, 0};  // S/dP issued into each buffer
-            for (int ks = 0;; ++ks) {
-                const int *h = sched_wait(sc, ks);
-                if (h[0] < 0) break;
-                const int cnt = h[3];
-                if (cnt > 0) {
-                    const int qb = nq & 1;
-                    mbar_wait(q_full + qb, (nq >> 1) & 1);
-                    tc_fence_after();
-                    ++nq;
-                    const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
-                    const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
-                    int prev_st = 0;
-                    for (int jj = 0; jj <= cnt; ++jj) {
-                        const int cur_st = st;
-                        if (jj < cnt) {  // S(jj), dP(jj) into buffer jj&1
-                            mbar_wait(kv_full + st, ph);
-                            tc_fence_after();
-                            const uint32_t cs = (jj & 1) * BUFW;
-                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
-                            const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * STG + KV_BYTES));
-                            if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
-                            ++nsb[jj & 1];
+        // MMA issuer: converged warp, one elected lane issues the tcgen05 instructions
+        int st = 0, nq = 0;
+        uint32_t ph = 0, ds_ph0 = 0, ds_ph1 = 0;
+        uint32_t nsb[2] = {0, 0};  // S/dP issued into each buffer
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int cnt = h[3];
+            if (cnt > 0) {
+                const int qb = nq & 1;
+                mbar_wait(q_full + qb, (nq >> 1) & 1);
+                tc_fence_after();
+                ++nq;
+                const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
+                const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
+                int prev_st = 0;
+                for (int jj = 0; jj <= cnt; ++jj) {
+                    const int cur_st = st;
+                    if (jj < cnt) {  // S(jj), dP(jj) into buffer jj&1
+                        mbar_wait(kv_full + st, ph);
+                        if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
+                        ++nsb[jj & 1];
+                        tc_fence_after();
+                        const uint32_t cs = (jj & 1) * BUFW;
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
+                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * STG + KV_BYTES));
+                        if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_bf16_ss(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
                             mma_commit(s_full + (jj & 1));
-                            if (++st == NST) { st = 0; ph ^= 1; }
                         }
-                        if (jj >= 1) {  // dQ += dS(jj-1) K(jj-1), dS from TMEM
-                            if ((jj - 1) & 1) { mbar_wait(ds_full + 1, ds_ph1); ds_ph1 ^= 1; }
-                            else { mbar_wait(ds_full + 0, ds_ph0); ds_ph0 ^= 1; }
-                            tc_fence_after();
-                            const uint32_t aS = tmem + ((jj - 1) & 1) * BUFW;
-                            const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + prev_st * STG));
+                        __syncwarp();
+                        if (++st == NST) { st = 0; ph ^= 1; }
+                    }
+                    if (jj >= 1) {  // dQ += dS(jj-1) K(jj-1), dS from TMEM
+                        if ((jj - 1) & 1) { mbar_wait(ds_full + 1, ds_ph1); ds_ph1 ^= 1; }
+                        else { mbar_wait(ds_full + 0, ds_ph0); ds_ph0 ^= 1; }
+                        tc_fence_after();
+                        const uint32_t aS = tmem + ((jj - 1) & 1) * BUFW;
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + prev_st * STG));
+                        if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
                                 mma_bf16_ts(tmem + COL_DQ, aS + 8 * k, dK0 + 128 * k, IDESC_DQ, (jj > 1) || (k > 0));
                             mma_commit(buf_free + ((jj - 1) & 1));
                             mma_commit(kv_empty + prev_st);
+                            if (jj == cnt) { mma_commit(dq_full); mma_commit(q_empty + qb); }
                         }
-                        prev_st = cur_st;
+                        __syncwarp();
                     }
-                    mma_commit(dq_full);
-                    mma_commit(q_empty + qb);
+                    prev_st = cur_st;
                 }
-                sched_release(sc, ks, false);
             }
+            sched_release(sc, ks, true);
         }
     } else {
         const int r = threadIdx.x;  // query row of the tile
@@ -773,53 +797,60 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *rows = sc.col + (ks & 3) * SCHED_CAP;
-            if (lane == 0 && cnt > 0) {
+            if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the copies
                 const int kb = nk & 1;
                 if (nk >= 2) mbar_wait(kv_empty + kb, ((nk >> 1) - 1) & 1);
-                mbar_arrive_expect_tx(kv_full + kb, 32768);
-                tma_load_3d(sKV + kb * 32768, &tmK, kv_full + kb, 0, t * 128, bh);
-                tma_load_3d(sKV + kb * 32768 + 16384, &tmV, kv_full + kb, 0, t * 128, bh);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(kv_full + kb, 32768);
+                    tma_load_3d(sKV + kb * 32768, &tmK, kv_full + kb, 0, t * 128, bh);
+                    tma_load_3d(sKV + kb * 32768 + 16384, &tmV, kv_full + kb, 0, t * 128, bh);
+                }
+                __syncwarp();
                 ++nk;
                 for (int j = 0; j < cnt; ++j) {
                     const int I = rows[j];
                     mbar_wait(q_empty + st, ph ^ 1);
                     uint8_t *stg = sStage + st * STAGE;
-                    mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
-                    tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
-                    tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
-                    bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
-                    bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
+                        tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
+                        tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
+                        bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                        bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                    }
+                    __syncwarp();
                     if (++st == NST) { st = 0; ph ^= 1; }
                 }
             }
             __syncwarp();
         }
     } else if (warp == 5) {
-        if (lane == 0) {
-            int ld_st = 0, use_st = 0, nk = 0;
-            uint32_t ld_ph = 0, p_ph0 = 0, p_ph1 = 0;
-            uint32_t nsb[2] = {0, 0};  // S^T/dP^T issued into each buffer
-            for (int ks = 0;; ++ks) {
-                const int *h = sched_wait(sc, ks);
-                if (h[0] < 0) break;
-                const int cnt = h[3];
-                if (cnt > 0) {
-                    const int kb = nk & 1;
-                    mbar_wait(kv_full + kb, (nk >> 1) & 1);
-                    tc_fence_after();
-                    ++nk;
-                    const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
-                    const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
-                    for (int jj = 0; jj <= cnt; ++jj) {
-                        if (jj < cnt) {  // S^T(jj), dP^T(jj) into buffer jj&1
-                            mbar_wait(q_full + ld_st, ld_ph);
-                            tc_fence_after();
-                            uint8_t *stg = sStage + ld_st * STAGE;
-                            const uint32_t cs = (jj & 1) * BUFW;
-                            const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
-                            const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
-                            if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
-                            ++nsb[jj & 1];
+        // MMA issuer: converged warp, one elected lane issues the tcgen05 instructions
+        int ld_st = 0, use_st = 0, nk = 0;
+        uint32_t ld_ph = 0, p_ph0 = 0, p_ph1 = 0;
+        uint32_t nsb[2] = {0, 0};  // S^T/dP^T issued into each buffer
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int cnt = h[3];
+            if (cnt > 0) {
+                const int kb = nk & 1;
+                mbar_wait(kv_full + kb, (nk >> 1) & 1);
+                tc_fence_after();
+                ++nk;
+                const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
+                const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
+                for (int jj = 0; jj <= cnt; ++jj) {
+                    if (jj < cnt) {  // S^T(jj), dP^T(jj) into buffer jj&1
+                        mbar_wait(q_full + ld_st, ld_ph);
+                        if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
+                        ++nsb[jj & 1];
+                        tc_fence_after();
+                        uint8_t *stg = sStage + ld_st * STAGE;
+                        const uint32_t cs = (jj & 1) * BUFW;
+                        const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
+                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                        if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
 #pragma unroll
@@ -827,17 +858,20 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                                 mma_bf16_ss(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
                             mma_commit(s_full + (jj & 1));
                             if (jj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
-                            if (++ld_st == NST) { ld_st = 0; ld_ph ^= 1; }
                         }
-                        if (jj >= 1) {  // dV += P^T dO, dK += dS^T Q for step jj-1 (A from TMEM)
-                            if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
-                            else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
-                            tc_fence_after();
-                            uint8_t *stg = sStage + use_st * STAGE;
-                            const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
-                            const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
-                            const uint32_t cs = ((jj - 1) & 1) * BUFW;
-                            const uint32_t acc = jj > 1;
+                        __syncwarp();
+                        if (++ld_st == NST) { ld_st = 0; ld_ph ^= 1; }
+                    }
+                    if (jj >= 1) {  // dV += P^T dO, dK += dS^T Q for step jj-1 (A from TMEM)
+                        if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
+                        else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
+                        tc_fence_after();
+                        uint8_t *stg = sStage + use_st * STAGE;
+                        const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
+                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                        const uint32_t cs = ((jj - 1) & 1) * BUFW;
+                        const uint32_t acc = jj > 1;
+                        if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
                                 mma_bf16_ts(tmem + COL_DV, tmem + cs + 8 * k, ddO0 + 128 * k, IDESC_DKV, acc || (k > 0));
@@ -846,13 +880,14 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                                 mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 8 * k, dQ0 + 128 * k, IDESC_DKV, acc || (k > 0));
                             mma_commit(buf_free + ((jj - 1) & 1));
                             mma_commit(q_empty + use_st);
-                            if (++use_st == NST) use_st = 0;
+                            if (jj == cnt) mma_commit(acc_full);
                         }
+                        __syncwarp();
+                        if (++use_st == NST) use_st = 0;
                     }
-                    mma_commit(acc_full);
                 }
-                sched_release(sc, ks, false);
             }
+            sched_release(sc, ks, true);
         }
     } else {
         const int r = threadIdx.x;  // key row of the tile = TMEM lane

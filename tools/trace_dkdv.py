@@ -21,7 +21,7 @@ lib.spion_debug_trace.restype = ctypes.c_int64
 buf = (ctypes.c_ulonglong * (3 * 2048))()
 n = lib.spion_debug_trace(buf, 3 * 2048)
 a = np.array(buf[:n], dtype=np.uint64).reshape(3, 1024, 2)
-names = {10: "P  q_empty ok", 20: "M  q_full ok", 21: "M  p_full ok", 30: "S  q_full ok", 31: "S  s_full ok", 32: "S  p arrive"}
+names = {10: "P  q_empty ok", 20: "M  q_full ok", 21: "M  buf_free ok (S issue)", 22: "M  p_full ok (dVdK issue)", 30: "S  step start", 31: "S  s_full ok", 32: "S  p arrive"}
 evs = []
 for role in range(3):
     for e, t in a[role]:
@@ -35,8 +35,7 @@ def times(code):
 a30, a31, a32 = times(30), times(31), times(32)
 m = min(len(a30), len(a31), len(a32))
 print("steps", m, "mean step us", np.diff(a32).mean() / 1000)
-print("S q_full->s_full", np.mean(a31[:m] - a30[:m]) / 1000, "s_full->p_arrive", np.mean(a32[:m] - a31[:m]) / 1000,
-      "p_arrive->next q_full", np.mean(a30[1:m] - a32[:m - 1]) / 1000)
-a20, a21 = times(20), times(21)
-m2 = min(len(a20), len(a21))
-print("M q_full->p_full", np.mean(a21[:m2] - a20[:m2]) / 1000, "M p_full->next q_full", np.mean(a20[1:m2] - a21[:m2 - 1]) / 1000)
+print("softmax: wait s_full", np.mean(a31[:m] - a30[:m]) / 1000, "compute", np.mean(a32[:m] - a31[:m]) / 1000)
+a20, a21, a22 = times(20), times(21), times(22)
+m2 = min(len(a20), len(a21), len(a22))
+print("MMA: q_full->buf_free", np.mean(a21[:m2] - a20[:m2]) / 1000)
