@@ -22,9 +22,10 @@
 //           -> dV += P^T dO_I, dK += dS^T Q_I (TMEM);  dK * scale -> bf16.
 //
 // Warp roles (192 threads): warps 0-3 softmax / epilogue (thread = TMEM lane =
-// tile row), warp 4 scheduler + TMA producer, warp 5 MMA issuer (one thread)
-// and TMEM allocator.  S (and dP) are double buffered in TMEM so the MMAs of the
-// next block overlap the softmax of the current one; P / dS are written back
+// tile row), warp 4 scheduler + TMA producer, warp 5 MMA issuer (one elected
+// lane of a converged warp) and TMEM allocator.  One CTA per SM owns all 512 TMEM
+// columns: S (and dP) rotate through NBUF buffers so the MMA warp runs up to NBUF
+// blocks ahead of the softmax warps; P / dS are written back
 // into TMEM as packed bf16 and consumed as the A operand of the next MMA
 // (tcgen05 TS form), so they never touch shared memory.  Per-item tiles (Q, or
 // K/V) are double buffered across work items.  Persistent grid; work items
@@ -43,17 +44,22 @@ namespace spion {
 using namespace tc;
 
 static constexpr int TC_THREADS = 192;
-// Per-B configuration.  B=32 kernels run 2 CTAs per SM (256 TMEM columns, ~113 KB of
-// shared memory each); the B=64 backward kernels need 512 TMEM columns for their
-// double-buffered S/dP and run 1 CTA per SM with deeper TMA rings instead.
+// Per-kernel, per-B configuration.  CTAS CTAs per SM share the 512 TMEM columns
+// (COLS each) and ~227 KB of shared memory; NBUF score buffers let the MMA warp run
+// up to NBUF blocks ahead of the softmax warps; TMA rings have NST >= NBUF stages
+// (which keeps the look-ahead deadlock free).  Two CTAs per SM where they fit (more
+// softmax warps per SM), one CTA with deeper buffering for the B=64 backward.
 template <int B> struct Cfg {
-    static constexpr int FWD_NST = B == 32 ? 8 : 4;   // K_J + V_J per stage
-    static constexpr int DQ_CTAS = B == 32 ? 2 : 1;
-    static constexpr int DQ_COLS = B == 32 ? 256 : 512;
-    static constexpr int DQ_NST = B == 32 ? 3 : 8;    // K_J + V_J per stage
-    static constexpr int DKV_CTAS = B == 32 ? 2 : 1;
-    static constexpr int DKV_COLS = B == 32 ? 256 : 512;
-    static constexpr int DKV_NST = B == 32 ? 4 : 8;   // Q_I + dO_I + lse_I + D_I per stage
+    static constexpr int FWD_CTAS = 2, FWD_COLS = 256;
+    static constexpr int FWD_NBUF = (256 - 64) / B;      // S/P buffers of B columns + O
+    static constexpr int FWD_NST = B == 32 ? 8 : 4;      // K_J + V_J per stage
+    static constexpr int DQ_CTAS = B == 32 ? 2 : 1, DQ_COLS = 512 / DQ_CTAS;
+    static constexpr int DQ_NBUF = (DQ_COLS - 64) / (2 * B);   // S+dP buffers + dQ
+    static constexpr int DQ_NST = B == 32 ? 3 : 8;             // K_J + V_J per stage
+    static constexpr int DKV_CTAS = B == 32 ? 2 : 1, DKV_COLS = 512 / DKV_CTAS;
+    static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
+    static constexpr int DKV_NST = B == 32 ? 4 : 9;              // Q_I + dO_I + lse_I + D_I per stage
+    static_assert(FWD_NST >= FWD_NBUF && DQ_NST >= DQ_NBUF && DKV_NST >= DKV_NBUF, "ring shallower than look-ahead");
 };
 static constexpr int SCHED_CAP = 128;  // max entries of one tile list (nblk <= 128)
 static constexpr float LOG2E = 1.4426950408889634f;
@@ -214,18 +220,19 @@ __device__ __forceinline__ void zero_row_bf16(__nv_bfloat16 *dst) {
 
 // ============================================================================ forward
 // Per (bh, row tile): Q tile double buffered across items; K_J/V_J stream through a
-// TMA ring; S_J lands in one of two TMEM buffers so the MMA for block J+1 runs
-// while the softmax warps work on block J; P_J (bf16) is written back over S_J in
-// TMEM and feeds O += P_J V_J as the A operand from tensor memory.
+// TMA ring; S_J lands in one of NBUF TMEM buffers so the MMA warp can run up to NBUF
+// blocks ahead of the softmax warps; P_J (bf16) is written back over S_J in TMEM and
+// feeds O += P_J V_J as the A operand from tensor memory.  Buffers rotate by a
+// global block counter g: buffer g % NBUF, use g / NBUF (mbarrier phase parity).
 template <int B>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+__global__ void __launch_bounds__(TC_THREADS, Cfg<B>::FWD_CTAS)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, TcParams p) {
-    constexpr int NST = Cfg<B>::FWD_NST;
+    constexpr int NST = Cfg<B>::FWD_NST, NBUF = Cfg<B>::FWD_NBUF;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;  // stage: K at +0, V at +KV_BYTES
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, 64, false, true);
-    constexpr uint32_t COL_O = 128;  // S / P buffer b at columns [64 b, 64 b + B)
+    constexpr uint32_t COL_O = NBUF * B;  // S / P buffer b at columns [B b, B b + B)
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
@@ -233,31 +240,23 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     uint8_t *sKV = smem + 32768;  // [NST] x STG
     uint8_t *sSched = sKV + NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    // p_full is per S/P buffer: the softmax may finish block J+1 before the MMA thread has
-    // observed block J, and one barrier would then run two phases ahead of its waiter
-    // pv_done[b]: the P.V MMA that read packed P from TMEM buffer b has completed.  The
-    // next S into b waits on it (the tensor pipe does not order an A-from-TMEM read
-    // against a later MMA's write of the same columns), and so do O rescales and the
-    // epilogue.  Per buffer, so no waiter can fall two phases behind (parity waits).
-    uint64_t *q_full = bars + 0, *q_empty = bars + 2, *p_full = bars + 4, *pv_done = bars + 6, *s_full = bars + 8,
-             *kv_full = bars + 11, *kv_empty = bars + 11 + NST;
-    Sched sc = make_sched(sSched, bars + 11 + 2 * NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 11 + 2 * NST + 8);
+    // s_full[b]: S in buffer b is ready; p_full[b]: packed P in buffer b is written;
+    // freeb[b]: the P.V that read buffer b completed (guards the next S into b, O rescales
+    // and the epilogue).  Per buffer, so no parity waiter can fall two phases behind.
+    uint64_t *q_full = bars + 0, *q_empty = bars + 2, *s_full = bars + 4, *p_full = s_full + NBUF,
+             *freeb = p_full + NBUF, *kv_full = freeb + NBUF, *kv_empty = kv_full + NST;
+    Sched sc = make_sched(sSched, kv_empty + NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(q_full + i, 1);
-            mbar_init(q_empty + i, 1);
-            mbar_init(s_full + i, 1);
-            mbar_init(p_full + i, 128);
-            mbar_init(pv_done + i, 1);
-        }
+        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); mbar_init(freeb + i, 1); }
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         sched_init(sc);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<256>(tmem_slot);
+    if (warp == 5) tmem_alloc<Cfg<B>::FWD_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -299,10 +298,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         }
     } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issuer (converged warp,
-        // one elected lane issues the tcgen05 instructions)
-        int st = 0, nq = 0;
-        uint32_t ph = 0, p_ph0 = 0, p_ph1 = 0;
-        uint32_t nsb[2] = {0, 0};  // S issued into each buffer
+        // one elected lane issues): S for up to NBUF blocks ahead, then P.V as P arrives
+        int sst = 0, pst = 0, nq = 0;  // ring cursors of the next S and the next P.V
+        uint32_t sph = 0;
+        uint32_t g = 0;                // global block counter (buffer = g % NBUF)
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -313,42 +312,41 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tc_fence_after();
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
-                int prev_st = 0;
-                for (int jj = 0; jj <= cnt; ++jj) {
-                    const int cur_st = st;
-                    if (jj < cnt) {  // S(jj) = Q K_J^T into buffer jj&1
-                        mbar_wait(kv_full + st, ph);
-                        if (nsb[jj & 1] > 0) mbar_wait(pv_done + (jj & 1), (nsb[jj & 1] - 1) & 1);
-                        ++nsb[jj & 1];
+                int sj = 0;  // next S of this item
+                for (int pj = 0; pj < cnt; ++pj) {
+                    for (; sj < cnt && sj < pj + NBUF; ++sj) {  // S(sj) = Q K_J^T into buffer (g+sj) % NBUF
+                        const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
+                        mbar_wait(kv_full + sst, sph);
+                        if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
                         tc_fence_after();
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
-                                mma_bf16_ss(tmem + (jj & 1) * 64, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
-                            mma_commit(s_full + (jj & 1));
-                            if (jj == cnt - 1) mma_commit(q_empty + qb);
+                                mma_bf16_ss(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                            mma_commit(s_full + b);
+                            if (sj == cnt - 1) mma_commit(q_empty + qb);
                         }
                         __syncwarp();
-                        if (++st == NST) { st = 0; ph ^= 1; }
+                        if (++sst == NST) { sst = 0; sph ^= 1; }
                     }
-                    if (jj >= 1) {  // O += P(jj-1) V(jj-1), P from TMEM
-                        if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
-                        else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
+                    {  // O += P(pj) V(pj), P from TMEM
+                        const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                        mbar_wait(p_full + b, u & 1);
                         tc_fence_after();
-                        const uint32_t aP = tmem + ((jj - 1) & 1) * 64;
-                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + prev_st * STG + KV_BYTES));
+                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + pst * STG + KV_BYTES));
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_O, aP + 8 * k, dV0 + 128 * k, IDESC_PV, (jj > 1) || (k > 0));
-                            mma_commit(pv_done + ((jj - 1) & 1));
-                            mma_commit(kv_empty + prev_st);
+                                mma_bf16_ts(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
+                            mma_commit(freeb + b);
+                            mma_commit(kv_empty + pst);
                         }
                         __syncwarp();
+                        if (++pst == NST) pst = 0;
                     }
-                    prev_st = cur_st;
                 }
+                g += cnt;
             }
             sched_release(sc, ks, true);
         }
@@ -357,8 +355,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const int r = threadIdx.x;  // tile row = TMEM lane
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t sph0 = 0, sph1 = 0;
-        uint32_t npv0 = 0, npv1 = 0;  // P.V MMAs on each buffer before the current item
+        uint32_t g = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
@@ -372,9 +369,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             float m_run = -INFINITY, l_run = 0.f;
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;  // warp-uniform (B >= 32)
-                const uint32_t sb = jj & 1;
-                if (sb == 0) { mbar_wait(s_full + 0, sph0); sph0 ^= 1; }
-                else { mbar_wait(s_full + 1, sph1); sph1 ^= 1; }
+                const uint32_t gs = g + jj, sb = gs % NBUF;
+                mbar_wait(s_full + sb, (gs / NBUF) & 1);
                 tc_fence_after();
                 uint32_t packed[B / 2];
                 float alpha = 1.f;
@@ -384,7 +380,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
                     for (int hh = 0; hh < B / 32; ++hh) {
                         float v[32];
-                        tmem_ld32(tl + sb * 64 + hh * 32, v);
+                        tmem_ld32(tl + sb * B + hh * 32, v);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; ++i) s[hh * 32 + i] = v[i] * sl2;
@@ -411,9 +407,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
                     for (int i = 0; i < B / 2; ++i) packed[i] = 0u;
                 }
-                if (__any_sync(0xffffffffu, rescale)) {  // O *= alpha once P.V(jj-1) is complete
-                    const int pj = jj - 1;  // P.V(pj) is the (npv_b + pj/2)-th on buffer pj&1
-                    mbar_wait(pv_done + (pj & 1), ((pj & 1 ? npv1 : npv0) + (pj >> 1)) & 1);
+                if (__any_sync(0xffffffffu, rescale)) {  // O *= alpha once every earlier P.V is complete
+                    for (int pj = (jj > NBUF ? jj - NBUF : 0); pj < jj; ++pj) {
+                        const uint32_t gp = g + pj;
+                        mbar_wait(freeb + gp % NBUF, (gp / NBUF) & 1);
+                    }
                     tc_fence_after();
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
@@ -430,7 +428,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     uint32_t v[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) v[i] = packed[hh * 16 + i];
-                    tmem_st16(tl + sb * 64 + hh * 16, v);
+                    tmem_st16(tl + sb * B + hh * 16, v);
                 }
                 tmem_st_wait();
                 tc_fence_before();
@@ -453,12 +451,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 f = exp2f(m_run - lse2);
             }
             if (cnt > 0) {
-                // the last P.V on each buffer: P.V(cnt-1) and P.V(cnt-2)
-                for (int pj = cnt - 1; pj >= 0 && pj >= cnt - 2; --pj)
-                    mbar_wait(pv_done + (pj & 1), ((pj & 1 ? npv1 : npv0) + (pj >> 1)) & 1);
+                // every P.V of the item that is not yet known complete (the last NBUF at most)
+                for (int pj = (cnt > NBUF ? cnt - NBUF : 0); pj < cnt; ++pj) {
+                    const uint32_t gp = g + pj;
+                    mbar_wait(freeb + gp % NBUF, (gp / NBUF) & 1);
+                }
                 tc_fence_after();
-                npv0 += (cnt + 1) >> 1;
-                npv1 += cnt >> 1;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     float o[32];
@@ -471,6 +469,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 zero_row_bf16(orow);
             }
             if (valid) p.lse_out[(int64_t)bh * p.L + row] = lse2 * LN2;
+            g += cnt;
             sched_release(sc, ks, true);
         }
     }
@@ -478,23 +477,22 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<Cfg<B>::FWD_COLS>(tmem);
     }
 }
 
 // ============================================================================ backward: dQ
 // Per (bh, row tile): D = rowsum(dO * O) (written for the dK/dV kernel); for each
-// block J: S, dP (double-buffered TMEM) -> dS = exp(S c - lse)(dP - D), packed bf16
-// over S in TMEM -> dQ += dS K_J (A from TMEM).  No atomics, no fp32 round trip.
+// block J: S, dP into one of NBUF TMEM buffer pairs -> dS = exp(S c - lse)(dP - D),
+// packed bf16 over S -> dQ += dS K_J (A from TMEM).  No atomics, no fp32 round trip.
 template <int B>
 __global__ void __launch_bounds__(TC_THREADS, Cfg<B>::DQ_CTAS)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, TcParams p) {
-    constexpr int NST = Cfg<B>::DQ_NST;
-    constexpr int COLS = Cfg<B>::DQ_COLS;
-    constexpr uint32_t BUFW = B == 32 ? 64 : 128;  // S at b*BUFW, dP at b*BUFW + B
-    constexpr uint32_t COL_DQ = 2 * BUFW;
+    constexpr int NST = Cfg<B>::DQ_NST, NBUF = Cfg<B>::DQ_NBUF;
+    constexpr uint32_t BUFW = 2 * B;  // S at b*BUFW, dP at b*BUFW + B
+    constexpr uint32_t COL_DQ = NBUF * BUFW;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);   // S = Q K^T, dP = dO V^T
     constexpr uint32_t IDESC_DQ = idesc_bf16(128, 64, false, true);  // dQ += dS K
@@ -505,21 +503,16 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     uint8_t *sKV = smem + 81920;                                    // [NST] x STG
     uint8_t *sSched = sKV + NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *q_full = bars + 0, *q_empty = bars + 2, *o_full = bars + 4, *o_empty = bars + 5, *s_full = bars + 6,
-             *ds_full = bars + 8 /*[2], per buffer*/, *dq_full = bars + 10, *buf_free = bars + 11 /*[2]*/,
-             *kv_full = bars + 13, *kv_empty = bars + 13 + NST;
-    Sched sc = make_sched(sSched, bars + 13 + 2 * NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 13 + 2 * NST + 8);
+    uint64_t *q_full = bars + 0, *q_empty = bars + 2, *o_full = bars + 4, *o_empty = bars + 5, *dq_full = bars + 6,
+             *s_full = bars + 7, *ds_full = s_full + NBUF, *freeb = ds_full + NBUF, *kv_full = freeb + NBUF,
+             *kv_empty = kv_full + NST;
+    Sched sc = make_sched(sSched, kv_empty + NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(q_full + i, 1);
-            mbar_init(q_empty + i, 1);
-            mbar_init(s_full + i, 1);
-            mbar_init(ds_full + i, 128);
-            mbar_init(buf_free + i, 1);
-        }
+        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(ds_full + i, 128); mbar_init(freeb + i, 1); }
         mbar_init(o_full, 1);
         mbar_init(o_empty, 128);
         mbar_init(dq_full, 1);
@@ -527,7 +520,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         sched_init(sc);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<COLS>(tmem_slot);
+    if (warp == 5) tmem_alloc<Cfg<B>::DQ_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -577,10 +570,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             __syncwarp();
         }
     } else if (warp == 5) {
-        // MMA issuer: converged warp, one elected lane issues the tcgen05 instructions
-        int st = 0, nq = 0;
-        uint32_t ph = 0, ds_ph0 = 0, ds_ph1 = 0;
-        uint32_t nsb[2] = {0, 0};  // S/dP issued into each buffer
+        // MMA issuer: converged warp, one elected lane issues; S/dP up to NBUF blocks ahead
+        int sst = 0, pst = 0, nq = 0;
+        uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -592,46 +584,45 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
                 const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
-                int prev_st = 0;
-                for (int jj = 0; jj <= cnt; ++jj) {
-                    const int cur_st = st;
-                    if (jj < cnt) {  // S(jj), dP(jj) into buffer jj&1
-                        mbar_wait(kv_full + st, ph);
-                        if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
-                        ++nsb[jj & 1];
+                int sj = 0;
+                for (int pj = 0; pj < cnt; ++pj) {
+                    for (; sj < cnt && sj < pj + NBUF; ++sj) {  // S(sj), dP(sj)
+                        const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
+                        mbar_wait(kv_full + sst, sph);
+                        if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
                         tc_fence_after();
-                        const uint32_t cs = (jj & 1) * BUFW;
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + st * STG));
-                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + st * STG + KV_BYTES));
+                        const uint32_t cs = b * BUFW;
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
+                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + sst * STG + KV_BYTES));
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_bf16_ss(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
-                            mma_commit(s_full + (jj & 1));
+                            mma_commit(s_full + b);
                         }
                         __syncwarp();
-                        if (++st == NST) { st = 0; ph ^= 1; }
+                        if (++sst == NST) { sst = 0; sph ^= 1; }
                     }
-                    if (jj >= 1) {  // dQ += dS(jj-1) K(jj-1), dS from TMEM
-                        if ((jj - 1) & 1) { mbar_wait(ds_full + 1, ds_ph1); ds_ph1 ^= 1; }
-                        else { mbar_wait(ds_full + 0, ds_ph0); ds_ph0 ^= 1; }
+                    {  // dQ += dS(pj) K(pj), dS from TMEM
+                        const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                        mbar_wait(ds_full + b, u & 1);
                         tc_fence_after();
-                        const uint32_t aS = tmem + ((jj - 1) & 1) * BUFW;
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + prev_st * STG));
+                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + pst * STG));
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DQ, aS + 8 * k, dK0 + 128 * k, IDESC_DQ, (jj > 1) || (k > 0));
-                            mma_commit(buf_free + ((jj - 1) & 1));
-                            mma_commit(kv_empty + prev_st);
-                            if (jj == cnt) { mma_commit(dq_full); mma_commit(q_empty + qb); }
+                                mma_bf16_ts(tmem + COL_DQ, tmem + b * BUFW + 8 * k, dK0 + 128 * k, IDESC_DQ, (pj > 0) || (k > 0));
+                            mma_commit(freeb + b);
+                            mma_commit(kv_empty + pst);
+                            if (pj == cnt - 1) { mma_commit(dq_full); mma_commit(q_empty + qb); }
                         }
                         __syncwarp();
+                        if (++pst == NST) pst = 0;
                     }
-                    prev_st = cur_st;
                 }
+                g += cnt;
             }
             sched_release(sc, ks, true);
         }
@@ -639,7 +630,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         const int r = threadIdx.x;  // query row of the tile
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t sph0 = 0, sph1 = 0, dq_ph = 0;
+        uint32_t dq_ph = 0, g = 0;
         int nq = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
@@ -668,8 +659,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const uint4 a = *reinterpret_cast<const uint4 *>(sO + sw128_offset(r, c));
-                    const uint4 g = *reinterpret_cast<const uint4 *>(rdO + sw128_offset(r, c));
-                    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
+                    const uint4 gg = *reinterpret_cast<const uint4 *>(rdO + sw128_offset(r, c));
+                    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {gg.x, gg.y, gg.z, gg.w};
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&av[i]));
@@ -682,9 +673,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             if (valid) p.D[(int64_t)bh * p.L + row] = Dr;
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;
-                const uint32_t sb = jj & 1;
-                if (sb == 0) { mbar_wait(s_full + 0, sph0); sph0 ^= 1; }
-                else { mbar_wait(s_full + 1, sph1); sph1 ^= 1; }
+                const uint32_t gs = g + jj, sb = gs % NBUF;
+                mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dQ MMA that read sb before
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
@@ -722,6 +712,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 if (valid) store_row_bf16(dqrow, v, p.scale, hh);
             }
             tc_fence_before();
+            g += cnt;
             sched_release(sc, ks, true);
         }
     }
@@ -729,27 +720,23 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc<COLS>(tmem);
+        tmem_dealloc<Cfg<B>::DQ_COLS>(tmem);
     }
 }
 
 // ============================================================================ backward: dK, dV
 // Per (bh, column tile): K/V tiles double buffered across items; for each query
-// block I: S^T, dP^T into one of two TMEM buffers (the MMA for I+1 overlaps the
-// softmax of I); P^T, dS^T packed over them feed dV += P^T dO_I, dK += dS^T Q_I
-// as A operands from tensor memory.
+// block I: S^T, dP^T into one of NBUF TMEM buffer pairs (the MMA warp runs up to NBUF
+// blocks ahead of the softmax warps); P^T, dS^T packed over them feed dV += P^T dO_I,
+// dK += dS^T Q_I as A operands from tensor memory.
 template <int B>
 __global__ void __launch_bounds__(TC_THREADS, Cfg<B>::DKV_CTAS)
 attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         TcParams p) {
-    constexpr int NST = Cfg<B>::DKV_NST;
-    constexpr int COLS = Cfg<B>::DKV_COLS;
-    constexpr uint32_t BUFW = B == 32 ? 64 : 128;  // S^T at b*BUFW, dP^T at b*BUFW + B
-    // dK accumulates at 2*BUFW and dV at 2*BUFW + 64.  (The mirrored placement, dV at
-    // column 256 fed from P^T at columns 0/128, produced corrupted dV rows on B200 for
-    // B=64 — test_bf16_parity[512-64-...] catches it; this order is verified.)
-    constexpr uint32_t COL_DK = 2 * BUFW, COL_DV = 2 * BUFW + 64;
+    constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF;
+    constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
+    constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;
     constexpr uint32_t TILE = B * 128;
     constexpr uint32_t STAGE = 2 * TILE + 1024;  // Q_I, dO_I, lse_I, D_I
     constexpr uint32_t IDESC_ST = idesc_bf16(128, B, false, false);   // S^T = K Q^T, dP^T = V dO^T
@@ -761,26 +748,21 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     uint8_t *sStage = smem + 65536;
     uint8_t *sSched = sStage + NST * STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *kv_full = bars + 0, *kv_empty = bars + 2, *s_full = bars + 4, *p_full = bars + 6 /*[2], per buffer*/,
-             *acc_full = bars + 8, *buf_free = bars + 9 /*[2]*/, *q_full = bars + 11, *q_empty = bars + 11 + NST;
-    Sched sc = make_sched(sSched, bars + 11 + 2 * NST);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 11 + 2 * NST + 8);
+    uint64_t *kv_full = bars + 0, *kv_empty = bars + 2, *acc_full = bars + 4, *s_full = bars + 5,
+             *p_full = s_full + NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
+    Sched sc = make_sched(sSched, q_empty + NST);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(kv_full + i, 1);
-            mbar_init(kv_empty + i, 1);
-            mbar_init(s_full + i, 1);
-            mbar_init(p_full + i, 128);
-            mbar_init(buf_free + i, 1);
-        }
+        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); mbar_init(freeb + i, 1); }
         mbar_init(acc_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
         sched_init(sc);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<COLS>(tmem_slot);
+    if (warp == 5) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -825,10 +807,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             __syncwarp();
         }
     } else if (warp == 5) {
-        // MMA issuer: converged warp, one elected lane issues the tcgen05 instructions
-        int ld_st = 0, use_st = 0, nk = 0;
-        uint32_t ld_ph = 0, p_ph0 = 0, p_ph1 = 0;
-        uint32_t nsb[2] = {0, 0};  // S^T/dP^T issued into each buffer
+        // MMA issuer: converged warp, one elected lane issues; S^T/dP^T up to NBUF blocks ahead
+        int sst = 0, pst = 0, nk = 0;
+        uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -840,14 +821,15 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 ++nk;
                 const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
-                for (int jj = 0; jj <= cnt; ++jj) {
-                    if (jj < cnt) {  // S^T(jj), dP^T(jj) into buffer jj&1
-                        mbar_wait(q_full + ld_st, ld_ph);
-                        if (nsb[jj & 1] > 0) mbar_wait(buf_free + (jj & 1), (nsb[jj & 1] - 1) & 1);
-                        ++nsb[jj & 1];
+                int sj = 0;
+                for (int pj = 0; pj < cnt; ++pj) {
+                    for (; sj < cnt && sj < pj + NBUF; ++sj) {  // S^T(sj), dP^T(sj)
+                        const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
+                        mbar_wait(q_full + sst, sph);
+                        if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
                         tc_fence_after();
-                        uint8_t *stg = sStage + ld_st * STAGE;
-                        const uint32_t cs = (jj & 1) * BUFW;
+                        uint8_t *stg = sStage + sst * STAGE;
+                        const uint32_t cs = b * BUFW;
                         const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
                         const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
                         if (elect_one()) {
@@ -856,36 +838,36 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_bf16_ss(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
-                            mma_commit(s_full + (jj & 1));
-                            if (jj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
+                            mma_commit(s_full + b);
+                            if (sj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
                         }
                         __syncwarp();
-                        if (++ld_st == NST) { ld_st = 0; ld_ph ^= 1; }
+                        if (++sst == NST) { sst = 0; sph ^= 1; }
                     }
-                    if (jj >= 1) {  // dV += P^T dO, dK += dS^T Q for step jj-1 (A from TMEM)
-                        if ((jj - 1) & 1) { mbar_wait(p_full + 1, p_ph1); p_ph1 ^= 1; }
-                        else { mbar_wait(p_full + 0, p_ph0); p_ph0 ^= 1; }
+                    {  // dV += P^T dO, dK += dS^T Q for block pj (A from TMEM)
+                        const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                        mbar_wait(p_full + b, u & 1);
                         tc_fence_after();
-                        uint8_t *stg = sStage + use_st * STAGE;
+                        uint8_t *stg = sStage + pst * STAGE;
                         const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
                         const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
-                        const uint32_t cs = ((jj - 1) & 1) * BUFW;
-                        const uint32_t acc = jj > 1;
+                        const uint32_t cs = b * BUFW;
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DV, tmem + cs + 8 * k, ddO0 + 128 * k, IDESC_DKV, acc || (k > 0));
+                                mma_bf16_ts(tmem + COL_DV, tmem + cs + 8 * k, ddO0 + 128 * k, IDESC_DKV, (pj > 0) || (k > 0));
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 8 * k, dQ0 + 128 * k, IDESC_DKV, acc || (k > 0));
-                            mma_commit(buf_free + ((jj - 1) & 1));
-                            mma_commit(q_empty + use_st);
-                            if (jj == cnt) mma_commit(acc_full);
+                                mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 8 * k, dQ0 + 128 * k, IDESC_DKV, (pj > 0) || (k > 0));
+                            mma_commit(freeb + b);
+                            mma_commit(q_empty + pst);
+                            if (pj == cnt - 1) mma_commit(acc_full);
                         }
                         __syncwarp();
-                        if (++use_st == NST) use_st = 0;
+                        if (++pst == NST) pst = 0;
                     }
                 }
+                g += cnt;
             }
             sched_release(sc, ks, true);
         }
@@ -893,7 +875,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         const int r = threadIdx.x;  // key row of the tile = TMEM lane
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t sph0 = 0, sph1 = 0, a_ph = 0, ph = 0;
+        uint32_t a_ph = 0, ph = 0, g = 0;
         int st = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
@@ -917,9 +899,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 mbar_wait(q_full + st, ph);  // lse_I, D_I
                 const float *slse = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
                 const float *sD = slse + 128;
-                const uint32_t sb = jj & 1;
-                if (sb == 0) { mbar_wait(s_full + 0, sph0); sph0 ^= 1; }
-                else { mbar_wait(s_full + 1, sph1); sph1 ^= 1; }
+                const uint32_t gs = g + jj, sb = gs % NBUF;
+                mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dV/dK MMAs that read sb before
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
@@ -966,6 +947,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 }
             }
             tc_fence_before();
+            g += cnt;
             sched_release(sc, ks, true);
         }
     }
@@ -973,7 +955,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     sched_finish(p);
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc<COLS>(tmem);
+        tmem_dealloc<Cfg<B>::DKV_COLS>(tmem);
     }
 }
 
@@ -1066,7 +1048,7 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     return p;
 }
 
-static const size_t SCHED_AREA = SCHED_BYTES + 256;
+static const size_t SCHED_AREA = SCHED_BYTES + 1024;  // scheduler ring + mbarriers + TMEM slot
 template <int B> static size_t fwd_smem() { return 1024 + 32768 + Cfg<B>::FWD_NST * 2 * B * 128 + SCHED_AREA; }
 template <int B> static size_t dq_smem() { return 1024 + 81920 + Cfg<B>::DQ_NST * 2 * B * 128 + SCHED_AREA; }
 template <int B> static size_t dkv_smem() { return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + SCHED_AREA; }
@@ -1088,10 +1070,10 @@ static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         !make_map(&mk, a.K, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
         !make_map(&mv, a.V, a.L, a.bh, a.stride_bh, a.stride_l, B))
         return SPION_ERR_CUDA;
-    TcParams p = base_params(a, 0, 2);
+    TcParams p = base_params(a, 0, Cfg<B>::FWD_CTAS);
     p.O = a.Oout;
     p.lse_out = a.lse_out;
-    attn_fwd_tc_kernel<B><<<grid_for(p, 2), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, p);
+    attn_fwd_tc_kernel<B><<<grid_for(p, Cfg<B>::FWD_CTAS), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, p);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
