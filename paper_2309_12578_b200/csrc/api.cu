@@ -28,6 +28,12 @@ int64_t spion_launch_count(void) { return (int64_t)g_launches.load(); }
 
 // debug: copy the event trace of the last traced kernel (SPION_TRACE=1) to host:
 // 3 roles (producer, MMA, softmax thread 0) x 1024 (event, globaltimer) pairs
+SPION_API int64_t spion_debug_k2_trace(unsigned long long *host) {
+    if (!spion::g_k2_trace) return 0;
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, spion::g_k2_trace, 8 * 8, cudaMemcpyDeviceToHost);
+    return 8;
+}
 SPION_API int64_t spion_debug_trace(unsigned long long *host, int64_t cap) {
     if (!spion::g_trace_buf) return 0;
     cudaDeviceSynchronize();

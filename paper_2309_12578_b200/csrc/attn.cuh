@@ -18,6 +18,7 @@ struct AttnArgs {
 };
 
 extern unsigned long long *g_trace_buf;  // debug event trace (SPION_TRACE=1)
+extern unsigned long long *g_k2_trace;   // debug K2 phase stamps (SPION_TRACE=1)
 
 bool simt_supported(int B, int d);
 spion_status launch_fwd_simt(const AttnArgs &a, spion_dtype dt, cudaStream_t s);

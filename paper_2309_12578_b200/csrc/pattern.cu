@@ -8,11 +8,15 @@
 //       pool(I,J) = sum_x sum_{f in F_I(x)} Wrow(x, J*B + f),
 //       F_I(x) = [max(x-IB-B+1, -h), min(x-IB, h)],  Wrow(x,s) = sum_{q<B} A(x, s+q)
 //    and a contiguous range of Wrow is a difference of the second row prefix
-//    sum PP.  One warp owns one source row segment at a time.
+//    sum PP.  One warp owns one source row segment at a time; the float4 loads
+//    of its next row are in flight while the current row is scanned.
 // K2 pattern_finalize_kernel (one CTA): threshold by exact order statistics,
-//    max-neighbour edges, flood fill as an anti-diagonal wavefront, forced
-//    diagonal, block-CSR/CSC and the attention work plan.
+//    max-neighbour edges as 128-bit row bitboards, flood fill as a row sweep
+//    (the reach along a row's right-edges is a carry chain: one 128-bit add),
+//    forced diagonal, block-CSR/CSC and the attention work plan from popcounts
+//    and bit scans.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -20,7 +24,8 @@ namespace spion {
 
 // ---------------------------------------------------------------- K1
 static constexpr int K1_WARPS = 8;
-static constexpr int K1_MAXP = 4;  // (target row, column) pairs per lane
+static constexpr int K1_MAXP = 4;   // (target row, column) pairs per lane
+static constexpr int K1_PREF = 6;   // float4 loads per lane kept in flight (covers W <= 768)
 
 struct K1Geom {
     int L, B, h, A, nI, JC, n_cc, W, CH;
@@ -63,10 +68,18 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
     unsigned long long *s_acc = reinterpret_cast<unsigned long long *>(k1_smem) + (size_t)K1_WARPS * ROW;
     const int npairs = g.nI * ncols;
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) s_acc[p] = 0ull;
+    for (int k = W + lane; k < ROW; k += 32) rowq[k] = 0ull;  // beyond the window: zero once
 
+    // loop-invariant (target row offset a, column jj) pairs of this lane
+    int pa[K1_MAXP], pj[K1_MAXP];
     unsigned long long acc[K1_MAXP];
 #pragma unroll
-    for (int t = 0; t < K1_MAXP; ++t) acc[t] = 0ull;
+    for (int t = 0; t < K1_MAXP; ++t) {
+        const int p = lane + 32 * t;
+        pa[t] = p < npairs ? p / ncols - g.A : (1 << 20);
+        pj[t] = p < npairs ? p % ncols : 0;
+        acc[t] = 0ull;
+    }
     bool bad = false;
 
     // float4 window covering [c0, c0+W)
@@ -74,62 +87,73 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
     const int n4 = (c0 + W - g4 + 3) >> 2;
     __syncthreads();
 
-    for (int u = warp; u < B; u += K1_WARPS) {
-        const int x = I0 * B + u;
-        const float *arow = A + (size_t)x * L;
-        // stage: coalesced float4 loads -> q (int64 fixed point) in smem, zero outside [0,L)
-        for (int k = lane; k < ROW; k += 32) rowq[k] = 0ull;
-        __syncwarp();
-        for (int v = lane; v < n4; v += 32) {
-            const int gc = g4 + 4 * v;
-            if (gc < 0 || gc >= L) continue;
-            float4 a4 = __ldg(reinterpret_cast<const float4 *>(arow + gc));
-            float av[4] = {a4.x, a4.y, a4.z, a4.w};
+    auto load4 = [&](const float *arow, int v) -> float4 {
+        const int gc = g4 + 4 * v;
+        return (v < n4 && gc >= 0 && gc < L) ? __ldg(reinterpret_cast<const float4 *>(arow + gc))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    // q (int64 fixed point, reading Q8) of one float4 into the row buffer; zero outside [0, L)
+    auto stage4 = [&](float4 f, int v) {
+        if (v >= n4) return;
+        const int gc = g4 + 4 * v;
+        const float av[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const int k = gc + t - c0;
-                if (k < 0 || k >= W) continue;
-                const float a = av[t];
-                if (!(a >= 0.f && a <= 1.f)) bad = true;
-                // a * 2^32 is exact in fp32; round half to even (reading Q8)
-                rowq[k] = (unsigned long long)__float2ll_rn(a * 4294967296.0f);
-            }
+        for (int t = 0; t < 4; ++t) {
+            const int k = gc + t - c0;
+            if (k < 0 || k >= W) continue;
+            const float a = av[t];
+            if (!(a >= 0.f && a <= 1.f)) bad = true;
+            // a * 2^32 is exact in fp32; round half to even
+            rowq[k] = (unsigned long long)__float2ll_rn(a * 4294967296.0f);
+        }
+    };
+
+    float4 cur[K1_PREF];
+    if (warp < B) {
+        const float *arow = A + (size_t)(I0 * B + warp) * L;
+#pragma unroll
+        for (int i = 0; i < K1_PREF; ++i) cur[i] = load4(arow, lane + 32 * i);
+    }
+    for (int u = warp; u < B; u += K1_WARPS) {
+        const float *arow = A + (size_t)(I0 * B + u) * L;
+#pragma unroll
+        for (int i = 0; i < K1_PREF; ++i) stage4(cur[i], lane + 32 * i);
+        for (int v = lane + 32 * K1_PREF; v < n4; v += 32) stage4(load4(arow, v), v);  // wide windows
+        if (u + K1_WARPS < B) {  // next row in flight during the scans below
+            const float *nrow = arow + (size_t)K1_WARPS * L;
+#pragma unroll
+            for (int i = 0; i < K1_PREF; ++i) cur[i] = load4(nrow, lane + 32 * i);
         }
         __syncwarp();
-        // pass A: chunk totals of q
+        // chunk totals of q and of sum_t q_t (CH-1-t), the chunk's contribution to the P sum
         const int k0 = lane * CH;
-        unsigned long long tot = 0;
-        for (int t = 0; t < CH; ++t) tot += rowq[k0 + t];
-        unsigned long long off = warp_excl_scan_u64(tot, lane);
-        // pass B: P[k] = sum_{c<k} q[c], in place; totals of P
-        unsigned long long run = off, tot2 = 0;
+        unsigned long long tot = 0, wsum = 0;
         for (int t = 0; t < CH; ++t) {
-            unsigned long long qv = rowq[k0 + t];
-            rowq[k0 + t] = run;
-            tot2 += run;
+            const unsigned long long qv = rowq[k0 + t];
+            tot += qv;
+            wsum += qv * (unsigned long long)(CH - 1 - t);
+        }
+        // P[k] = sum_{c<k} q[c] (P at chunk start: off1); PP[k] = sum_{k'<k} P[k'] (in place)
+        const unsigned long long off1 = warp_excl_scan_u64(tot, lane);
+        const unsigned long long off2 = warp_excl_scan_u64((unsigned long long)CH * off1 + wsum, lane);
+        unsigned long long run = off1, run2 = off2;
+        for (int t = 0; t < CH; ++t) {
+            const unsigned long long qv = rowq[k0 + t];
+            rowq[k0 + t] = run2;
+            run2 += run;
             run += qv;
         }
-        unsigned long long off2 = warp_excl_scan_u64(tot2, lane);
-        // pass C: PP[k] = sum_{k'<k} P[k'], in place
-        unsigned long long run2 = off2;
-        for (int t = 0; t < CH; ++t) {
-            unsigned long long pv = rowq[k0 + t];
-            rowq[k0 + t] = run2;
-            run2 += pv;
-        }
         __syncwarp();
-        // contributions of row x to pool rows I0+a, columns J0+jj
+        // contributions of row x = I0*B+u to pool rows I0+a, columns J0+jj
 #pragma unroll
         for (int t = 0; t < K1_MAXP; ++t) {
-            const int p = lane + 32 * t;
-            if (p >= npairs) break;
-            const int a = p / ncols - g.A, jj = p % ncols;
+            const int a = pa[t];
             const int I = I0 + a;
             if (I < 0 || I >= n) continue;
             const int r = u - a * B;
             const int f0 = max(r - B + 1, -h), f1 = min(r, h);
             if (f0 > f1) continue;
-            const int s0 = jj * B + h + f0, s1 = jj * B + h + f1;
+            const int s0 = pj[t] * B + h + f0, s1 = pj[t] * B + h + f1;
             acc[t] += (rowq[s1 + 1 + B] - rowq[s0 + B]) - (rowq[s1 + 1] - rowq[s0]);
         }
         __syncwarp();
@@ -151,6 +175,40 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
 
 // ---------------------------------------------------------------- K2
 static constexpr int K2_THREADS = 1024;
+static constexpr int K2_MAXN = 128;  // n = L/B <= 128: one row of the block grid is 4 x 32 bits
+
+// 128-bit row bitboard (bit c = block column c)
+struct Bits {
+    unsigned long long lo, hi;
+};
+__device__ __forceinline__ Bits b_and(Bits a, Bits b) { return {a.lo & b.lo, a.hi & b.hi}; }
+__device__ __forceinline__ Bits b_or(Bits a, Bits b) { return {a.lo | b.lo, a.hi | b.hi}; }
+__device__ __forceinline__ Bits b_xor(Bits a, Bits b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
+__device__ __forceinline__ Bits b_shl1(Bits a) { return {a.lo << 1, (a.hi << 1) | (a.lo >> 63)}; }
+__device__ __forceinline__ Bits b_add(Bits a, Bits b) {
+    const unsigned long long lo = a.lo + b.lo;
+    return {lo, a.hi + b.hi + (lo < a.lo ? 1ull : 0ull)};
+}
+__device__ __forceinline__ Bits b_bit(int c) {
+    return c < 64 ? Bits{1ull << c, 0ull} : Bits{0ull, 1ull << (c - 64)};
+}
+__device__ __forceinline__ Bits b_ones(int n) {  // bits [0, n), 1 <= n <= 128
+    if (n >= 128) return {~0ull, ~0ull};
+    if (n > 64) return {~0ull, ~0ull >> (128 - n)};
+    return {~0ull >> (64 - n), 0ull};
+}
+__device__ __forceinline__ int b_popc(Bits a) { return __popcll(a.lo) + __popcll(a.hi); }
+// the row bitboard stored as 4 x 32-bit ballot words in shared memory
+__device__ __forceinline__ Bits b_load(const unsigned *w) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(w);
+    return {(unsigned long long)v.x | ((unsigned long long)v.y << 32),
+            (unsigned long long)v.z | ((unsigned long long)v.w << 32)};
+}
+__device__ __forceinline__ void b_store(unsigned *w, Bits a) {
+    *reinterpret_cast<uint4 *>(w) =
+        make_uint4((unsigned)a.lo, (unsigned)(a.lo >> 32), (unsigned)a.hi, (unsigned)(a.hi >> 32));
+}
+__device__ __forceinline__ unsigned b_get(const unsigned *w, int c) { return (w[c >> 5] >> (c & 31)) & 1u; }
 
 // k-th smallest (0-based) of v[0..N) by MSD radix selection, 8-bit digits.
 __device__ long long block_select_kth(const long long *v, int N, long long k, unsigned int *hist,
@@ -187,116 +245,6 @@ __device__ long long block_select_kth(const long long *v, int N, long long k, un
     return (long long)prefix;
 }
 
-// BSR / CSC / plan from the block mask in shared memory (fl: n*n bytes).
-__device__ void build_bsr_and_plan(const uint8_t *fl, int n, int block, int *brow_ptr, int *bcol_idx,
-                                   int *bcol_ptr, int *brow_idx, uint8_t *mask_out, int *nnzb_out,
-                                   int nnzb_cap, int *plan, int *flags, int *s_cnt, int *s_off) {
-    const int tid = threadIdx.x;
-    for (int i = tid; mask_out && i < n * n; i += blockDim.x) mask_out[i] = fl[i];
-    // row and column counts
-    for (int r = tid; r < 2 * n; r += blockDim.x) {
-        int c = 0;
-        if (r < n) { for (int j = 0; j < n; ++j) c += fl[r * n + j]; }
-        else { int col = r - n; for (int i = 0; i < n; ++i) c += fl[i * n + col]; }
-        s_cnt[r] = c;
-    }
-    __syncthreads();
-    if (tid < 32) {  // exclusive scans of the two count arrays (n <= 128 -> <= 4 per lane)
-        for (int which = 0; which < 2; ++which) {
-            const int *cnt = s_cnt + which * n;
-            int *off = s_off + which * (n + 1);
-            int per = (n + 31) / 32;
-            int loc = 0;
-            for (int t = 0; t < per; ++t) { int r = tid * per + t; if (r < n) loc += cnt[r]; }
-            int ex = warp_excl_scan_i32(loc, tid);
-            for (int t = 0; t < per; ++t) { int r = tid * per + t; if (r < n) { off[r] = ex; ex += cnt[r]; } }
-            if (tid == 31) off[n] = ex;
-        }
-    }
-    __syncthreads();
-    const int nnzb = s_off[n];
-    if (tid == 0) {
-        *nnzb_out = nnzb;
-        if (nnzb > nnzb_cap && flags) atomicOr(flags, FLAG_CAPACITY);
-    }
-    for (int r = tid; r <= n; r += blockDim.x) { brow_ptr[r] = s_off[r]; bcol_ptr[r] = s_off[n + 1 + r]; }
-    for (int r = tid; r < 2 * n; r += blockDim.x) {
-        if (r < n) {
-            int o = s_off[r];
-            for (int j = 0; j < n; ++j)
-                if (fl[r * n + j]) { if (o < nnzb_cap) bcol_idx[o] = j; ++o; }
-        } else {
-            int col = r - n;
-            int o = s_off[n + 1 + col];
-            for (int i = 0; i < n; ++i)
-                if (fl[i * n + col]) { if (o < nnzb_cap) brow_idx[o] = i; ++o; }
-        }
-    }
-    // attention work plan: slot tiles of S consecutive block rows (fwd) / columns (bwd)
-    if (plan) {
-        PlanLayout pl(n, block);
-        __syncthreads();
-        for (int t = tid; t < 2 * pl.ntiles; t += blockDim.x) {
-            const bool fwd = t < pl.ntiles;
-            const int tt = fwd ? t : t - pl.ntiles;
-            int c = 0;
-            for (int j = 0; j < n; ++j) {
-                int m = 0;
-                for (int s = 0; s < pl.S; ++s) {
-                    int r = tt * pl.S + s;
-                    if (r < n && (fwd ? fl[r * n + j] : fl[j * n + r])) m |= 1 << s;
-                }
-                c += (m != 0);
-            }
-            s_cnt[t] = c;
-        }
-        __syncthreads();
-        if (tid < 32) {
-            for (int which = 0; which < 2; ++which) {
-                const int *cnt = s_cnt + which * pl.ntiles;
-                int *ptr = plan + (which ? pl.bptr : pl.fptr);
-                int per = (pl.ntiles + 31) / 32;
-                int loc = 0;
-                for (int q = 0; q < per; ++q) { int r = tid * per + q; if (r < pl.ntiles) loc += cnt[r]; }
-                int ex = warp_excl_scan_i32(loc, tid);
-                for (int q = 0; q < per; ++q) { int r = tid * per + q; if (r < pl.ntiles) { ptr[r] = ex; s_off[which * (pl.ntiles + 1) + r] = ex; ex += cnt[r]; } }
-                if (tid == 31) { ptr[pl.ntiles] = ex; plan[3 + which] = ex; }
-            }
-            if (tid == 0) {
-                plan[0] = n; plan[1] = pl.S; plan[2] = pl.ntiles;
-                for (int w = 5; w < 16; ++w) plan[w] = 0;  // scheduler counters start at zero
-            }
-        }
-        __syncthreads();
-        // tiles in descending order of work (stable): the attention kernels hand out the
-        // longest tiles of a bh-chunk first (longest-processing-time-first scheduling)
-        for (int t = tid; t < 2 * pl.ntiles; t += blockDim.x) {
-            const bool fwd = t < pl.ntiles;
-            const int tt = fwd ? t : t - pl.ntiles;
-            const int *cnt = s_cnt + (fwd ? 0 : pl.ntiles);
-            const int c = cnt[tt];
-            int rank = 0;
-            for (int u = 0; u < pl.ntiles; ++u) rank += (cnt[u] > c) || (cnt[u] == c && u < tt);
-            plan[(fwd ? pl.forder : pl.border) + rank] = tt;
-        }
-        for (int t = tid; t < 2 * pl.ntiles; t += blockDim.x) {
-            const bool fwd = t < pl.ntiles;
-            const int tt = fwd ? t : t - pl.ntiles;
-            int o = s_off[(fwd ? 0 : 1) * (pl.ntiles + 1) + tt];
-            int *col = plan + (fwd ? pl.fcol : pl.brow);
-            int *msk = plan + (fwd ? pl.fmsk : pl.bmsk);
-            for (int j = 0; j < n; ++j) {
-                int m = 0;
-                for (int s = 0; s < pl.S; ++s) {
-                    int r = tt * pl.S + s;
-                    if (r < n && (fwd ? fl[r * n + j] : fl[j * n + r])) m |= 1 << s;
-                }
-                if (m) { col[o] = j; msk[o] = m; ++o; }
-            }
-        }
-    }
-}
-
 struct K2Args {
     const long long *pool;  // [n][n] fixed-point pool sums
     int n, block;
@@ -309,24 +257,176 @@ struct K2Args {
     uint8_t *mask;
     int nnzb_cap;
     int *plan;
+    unsigned long long *trace;  // debug (SPION_TRACE=1): phase timestamps
 };
+
+__device__ __forceinline__ void k2_stamp(const K2Args &a, int k) {
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[k] = t;
+    }
+}
+
+// shared scratch of the BSR / plan builder
+struct K2Scratch {
+    unsigned *flw;   // [K2_MAXN][4] row bitboards of the final block mask
+    unsigned *colw;  // [K2_MAXN][4] column bitboards (bit r of column c)
+    int *cnt;        // [2 * K2_MAXN]
+    int *off;        // [2 * (K2_MAXN + 1)]
+};
+
+// exclusive scans of cnt[0..m) and cnt[m..2m) into off[0..m] and off[m+1..2m+1]; warp 0 only
+__device__ void scan2(const int *cnt, int *off, int m) {
+    const int lane = threadIdx.x & 31;
+    const int per = (m + 31) / 32;
+    for (int which = 0; which < 2; ++which) {
+        const int *c = cnt + which * m;
+        int *o = off + which * (m + 1);
+        int loc = 0;
+        for (int t = 0; t < per; ++t) { const int r = lane * per + t; if (r < m) loc += c[r]; }
+        int ex = warp_excl_scan_i32(loc, lane);
+        for (int t = 0; t < per; ++t) { const int r = lane * per + t; if (r < m) { o[r] = ex; ex += c[r]; } }
+        if (lane == 31) o[m] = ex;
+    }
+}
+
+// Block-CSR / CSC / plan from the row bitboards sc.flw (all threads of the CTA).
+__device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
+    const int n = a.n, tid = threadIdx.x, nthr = blockDim.x;
+    // column bitboards: thread c gathers bit c of every row (warp-uniform broadcast reads)
+    for (int c = tid; c < n; c += nthr) {
+        unsigned w[4] = {0u, 0u, 0u, 0u};
+        const int cw = c >> 5, cb = c & 31;
+        for (int r = 0; r < n; ++r) w[r >> 5] |= ((sc.flw[r * 4 + cw] >> cb) & 1u) << (r & 31);
+        *reinterpret_cast<uint4 *>(sc.colw + c * 4) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __syncthreads();
+    for (int r = tid; r < 2 * n; r += nthr)
+        sc.cnt[r] = b_popc(b_load(r < n ? sc.flw + r * 4 : sc.colw + (r - n) * 4));
+    __syncthreads();
+    if (tid < 32) scan2(sc.cnt, sc.off, n);
+    __syncthreads();
+    const int nnzb = sc.off[n];
+    if (tid == 0) {
+        *a.nnzb = nnzb;
+        if (nnzb > a.nnzb_cap && a.flags) atomicOr(a.flags, FLAG_CAPACITY);
+    }
+    for (int r = tid; r <= n; r += nthr) { a.brow_ptr[r] = sc.off[r]; a.bcol_ptr[r] = sc.off[n + 1 + r]; }
+    // ascending column (row) indices by scanning the set bits
+    for (int r = tid; r < 2 * n; r += nthr) {
+        const bool row = r < n;
+        const Bits m = b_load(row ? sc.flw + r * 4 : sc.colw + (r - n) * 4);
+        int o = row ? sc.off[r] : sc.off[n + 1 + (r - n)];
+        int *dst = row ? a.bcol_idx : a.brow_idx;
+        for (int half = 0; half < 2; ++half) {
+            unsigned long long w = half ? m.hi : m.lo;
+            while (w) {
+                const int j = half * 64 + __ffsll((long long)w) - 1;
+                w &= w - 1;
+                if (o < a.nnzb_cap) dst[o] = j;
+                ++o;
+            }
+        }
+    }
+    if (a.mask) {
+        const int N = n * n;
+        for (int i = tid; i < N; i += nthr) a.mask[i] = (uint8_t)b_get(sc.flw + (i / n) * 4, i % n);
+    }
+    if (!a.plan) return;
+    // attention work plan: slot tiles of S consecutive block rows (fwd) / block columns (bwd);
+    // one entry per column (row) in the union of the tile's S rows (columns), with a slot mask
+    const PlanLayout pl(n, a.block);
+    int *plan = a.plan;
+    __syncthreads();
+    for (int t = tid; t < 2 * pl.ntiles; t += nthr) {
+        const bool fwd = t < pl.ntiles;
+        const int tt = fwd ? t : t - pl.ntiles;
+        const unsigned *src = fwd ? sc.flw : sc.colw;
+        Bits u{0ull, 0ull};
+        for (int s = 0; s < pl.S; ++s) {
+            const int r = tt * pl.S + s;
+            if (r < n) u = b_or(u, b_load(src + r * 4));
+        }
+        sc.cnt[t] = b_popc(u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+        scan2(sc.cnt, sc.off, pl.ntiles);
+        for (int r = tid; r <= pl.ntiles; r += 32) {
+            plan[pl.fptr + r] = sc.off[r];
+            plan[pl.bptr + r] = sc.off[pl.ntiles + 1 + r];
+        }
+        if (tid == 0) {
+            plan[0] = n; plan[1] = pl.S; plan[2] = pl.ntiles;
+            plan[3] = sc.off[pl.ntiles];
+            plan[4] = sc.off[2 * pl.ntiles + 1];
+            for (int w = 5; w < 16; ++w) plan[w] = 0;  // scheduler counters start at zero
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < 2 * pl.ntiles; t += nthr) {
+        const bool fwd = t < pl.ntiles;
+        const int tt = fwd ? t : t - pl.ntiles;
+        const unsigned *src = fwd ? sc.flw : sc.colw;
+        // tiles in descending order of work (stable): the attention kernels hand out the
+        // longest tiles of a bh-chunk first (longest-processing-time-first scheduling)
+        const int *cnt = sc.cnt + (fwd ? 0 : pl.ntiles);
+        const int c = cnt[tt];
+        int rank = 0;
+        for (int v = 0; v < pl.ntiles; ++v) rank += (cnt[v] > c) || (cnt[v] == c && v < tt);
+        plan[(fwd ? pl.forder : pl.border) + rank] = tt;
+        Bits u{0ull, 0ull};
+        for (int s = 0; s < pl.S; ++s) {
+            const int r = tt * pl.S + s;
+            if (r < n) u = b_or(u, b_load(src + r * 4));
+        }
+        int o = sc.off[(fwd ? 0 : pl.ntiles + 1) + tt];
+        int *col = plan + (fwd ? pl.fcol : pl.brow);
+        int *msk = plan + (fwd ? pl.fmsk : pl.bmsk);
+        for (int half = 0; half < 2; ++half) {
+            unsigned long long w = half ? u.hi : u.lo;
+            while (w) {
+                const int j = half * 64 + __ffsll((long long)w) - 1;
+                w &= w - 1;
+                int m = 0;
+                for (int s = 0; s < pl.S; ++s) {
+                    const int r = tt * pl.S + s;
+                    if (r < n) m |= (int)b_get(src + r * 4, j) << s;
+                }
+                col[o] = j;
+                msk[o] = m;
+                ++o;
+            }
+        }
+    }
+}
+
+static __host__ __device__ constexpr int k2_bits_words() { return 4 * K2_MAXN; }
 
 __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
-    const int n = a.n, N = n * n, tid = threadIdx.x;
+    const int n = a.n, N = n * n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     long long *s_pool = reinterpret_cast<long long *>(k2_smem);
-    const int N16 = (N + 15) & ~15;
-    uint8_t *s_cell = reinterpret_cast<uint8_t *>(s_pool + N);
-    uint8_t *s_fl = s_cell + N16;
-    int *s_cnt = reinterpret_cast<int *>(s_fl + N16);
-    int *s_off = s_cnt + 2 * n + 8;
-    unsigned int *hist = reinterpret_cast<unsigned int *>(s_off + 2 * (n + 1) + 8);
+    unsigned *gtw = reinterpret_cast<unsigned *>(s_pool + ((N + 1) & ~1));  // [n][4] row bitboards: > t
+    unsigned *dnw = gtw + k2_bits_words();                      // edge (r,c) -> (r+1,c)
+    unsigned *rtw = dnw + k2_bits_words();                      // edge (r,c) -> (r,c+1)
+    unsigned *dgw = rtw + k2_bits_words();                      // edge (r,c) -> (r+1,c+1)
+    K2Scratch sc;
+    sc.flw = dgw + k2_bits_words();
+    sc.colw = sc.flw + k2_bits_words();
+    sc.cnt = reinterpret_cast<int *>(sc.colw + k2_bits_words());
+    sc.off = sc.cnt + 2 * K2_MAXN + 8;
+    unsigned int *hist = reinterpret_cast<unsigned int *>(sc.off + 2 * (K2_MAXN + 1) + 8);
     __shared__ long long bc[4];
     __shared__ unsigned long long s_red[2];
+    __shared__ unsigned int s_le;
 
+    k2_stamp(a, 0);
     for (int i = tid; i < N; i += blockDim.x) s_pool[i] = a.pool[i];
-    if (tid == 0) { s_red[0] = 0ull; s_red[1] = ~0ull; }
+    if (tid == 0) { s_red[0] = 0ull; s_red[1] = ~0ull; s_le = 0u; }
     __syncthreads();
+    k2_stamp(a, 1);
 
     // ---- threshold as an integer T: gt(x) <=> x > T (reading Q9)
     long long T;
@@ -336,7 +436,7 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
         unsigned long long orv = 0;
         for (int i = tid; i < N; i += blockDim.x) orv |= (unsigned long long)s_pool[i];
         for (int o = 16; o > 0; o >>= 1) orv |= __shfl_xor_sync(0xffffffffu, orv, o);
-        if ((tid & 31) == 0 && orv) atomicOr(&s_red[0], orv);
+        if (lane == 0 && orv) atomicOr(&s_red[0], orv);
         __syncthreads();
         const unsigned long long all = s_red[0];
         const int topbit = all ? 63 - __clzll((long long)all) : 0;
@@ -351,9 +451,6 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
                 long long x = s_pool[i];
                 if (x <= v_lo) ++le; else mn = min(mn, (unsigned long long)x);
             }
-            __shared__ unsigned int s_le;
-            if (tid == 0) s_le = 0;
-            __syncthreads();
             atomicAdd(&s_le, le);
             atomicMin(&s_red[1], mn);
             __syncthreads();
@@ -363,94 +460,107 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
             T = v_lo;
         }
     }
+    k2_stamp(a, 2);
 
-    // ---- gt and max-neighbour edges (Alg. 4 l.3-15)
-    for (int i = tid; i < N; i += blockDim.x) {
-        const int r = i / n, c = i % n;
-        uint8_t f = (s_pool[i] > T) ? 1 : 0;
-        if (r + 1 < n && c + 1 < n) {  // Alg. 4 l.1: last row / column has no out-edges
-            const long long below = s_pool[i + n], right = s_pool[i + 1], diag = s_pool[i + n + 1];
-            long long m = below > right ? below : right;
-            m = m > diag ? m : diag;
-            if (below == m) f |= 2;
-            if (right == m) f |= 4;
-            if (diag == m) f |= 8;
-        }
-        s_cell[i] = f;
-    }
-    __syncthreads();
-
-    // ---- flood fill: reach from the seeds row 0 / column 0 (Alg. 3 l.5-8) along the edges,
-    //      anti-diagonal by anti-diagonal (every edge goes from r+c to r+c+1 or r+c+2)
-    const int nw = ((n + 31) / 32) * 32;
-    if (tid < nw) {
-        for (int d = 0; d <= 2 * n - 2; ++d) {
-            const int r = tid, c = d - tid;
-            if (r < n && c >= 0 && c < n) {
-                bool inr = false;
-                if (r > 0 && (s_cell[(r - 1) * n + c] & (16 | 2)) == (16 | 2)) inr = true;
-                if (c > 0 && (s_cell[r * n + c - 1] & (16 | 4)) == (16 | 4)) inr = true;
-                if (r > 0 && c > 0 && (s_cell[(r - 1) * n + c - 1] & (16 | 8)) == (16 | 8)) inr = true;
-                uint8_t f = s_cell[r * n + c];
-                if (inr) f |= 32;
-                if (inr || r == 0 || c == 0) f |= 16;  // visited
-                s_cell[r * n + c] = f;
+    // ---- gt and max-neighbour edges (Alg. 4 l.1-15) as row bitboards: one warp per 32-bit word
+    for (int pw = warp; pw < n * 4; pw += K2_THREADS / 32) {
+        const int r = pw >> 2, c = (pw & 3) * 32 + lane;
+        bool g = false, dn = false, rt = false, dg = false;
+        if (c < n) {
+            const long long v = s_pool[r * n + c];
+            g = v > T;
+            if (r + 1 < n && c + 1 < n) {  // Alg. 4 l.1: the last row / column has no out-edges
+                const long long below = s_pool[(r + 1) * n + c], right = s_pool[r * n + c + 1],
+                                diag = s_pool[(r + 1) * n + c + 1];
+                long long m = below > right ? below : right;
+                m = m > diag ? m : diag;
+                dn = below == m;
+                rt = right == m;
+                dg = diag == m;
             }
-            asm volatile("bar.sync 1, %0;" ::"r"(nw) : "memory");
+        }
+        const unsigned bg = __ballot_sync(0xffffffffu, g), bd = __ballot_sync(0xffffffffu, dn),
+                       br = __ballot_sync(0xffffffffu, rt), bq = __ballot_sync(0xffffffffu, dg);
+        if (lane == 0) { gtw[pw] = bg; dnw[pw] = bd; rtw[pw] = br; dgw[pw] = bq; }
+    }
+    __syncthreads();
+    k2_stamp(a, 3);
+
+    // ---- flood fill: reach from the seeds (0, i), (j, 0) (Alg. 3 l.5-8) along the edges, row by row.
+    //   E_r   = cells of row r entered from row r-1 (down edges, diagonal edges shifted by one)
+    //   reach along row r's right edges: R[c] = X[c] | (R[c-1] & rt[c-1]) with X = E_r + seeds.
+    //   That recurrence is a carry chain: with g = X & rt, p = rt the carries of g + p are
+    //   C[c] = R[c-1] & rt[c-1] (the cells entered by a right edge); R = X | C.
+    //   marked = (entered by an edge AND > t) (Alg. 4 l.5-7) OR diagonal (Alg. 3 l.9-10)
+    if (tid == 0) {
+        const Bits all = b_ones(n);
+        Bits vis{0ull, 0ull}, dn{0ull, 0ull}, dg{0ull, 0ull};
+#pragma unroll 4
+        for (int r = 0; r < n; ++r) {
+            const Bits rt = b_load(rtw + r * 4), gt = b_load(gtw + r * 4);
+            const Bits E = b_or(b_and(vis, dn), b_shl1(b_and(vis, dg)));
+            const Bits X = b_or(E, r == 0 ? all : Bits{1ull, 0ull});
+            const Bits gg = b_and(X, rt);
+            const Bits C = b_xor(b_add(gg, rt), b_xor(gg, rt));
+            vis = b_or(X, C);
+            const Bits fl = b_or(b_and(b_or(E, C), gt), b_bit(r));
+            b_store(sc.flw + r * 4, fl);
+            dn = b_load(dnw + r * 4);
+            dg = b_load(dgw + r * 4);
         }
     }
     __syncthreads();
-    // marked = reached by an edge and > t (Alg. 4 l.5-7), plus the forced diagonal (Alg. 3 l.9-10)
-    for (int i = tid; i < N; i += blockDim.x) {
-        const int r = i / n, c = i % n;
-        const uint8_t f = s_cell[i];
-        s_fl[i] = (((f & 32) && (f & 1)) || r == c) ? 1 : 0;
-    }
+    k2_stamp(a, 4);
+    k2_stamp(a, 5);
+    build_bsr_and_plan(a, sc);
     __syncthreads();
-    build_bsr_and_plan(s_fl, n, a.block, a.brow_ptr, a.bcol_idx, a.bcol_ptr, a.brow_idx, a.mask, a.nnzb,
-                       a.nnzb_cap, a.plan, a.flags, s_cnt, s_off);
+    k2_stamp(a, 6);
 }
 
 __global__ void __launch_bounds__(K2_THREADS) bsr_from_mask_kernel(const uint8_t *mask_in, K2Args a) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
-    const int n = a.n, N = n * n, tid = threadIdx.x;
-    uint8_t *s_fl = k2_smem;
-    int *s_cnt = reinterpret_cast<int *>(s_fl + ((N + 15) & ~15));
-    int *s_off = s_cnt + 2 * n + 8;
+    const int n = a.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    K2Scratch sc;
+    sc.flw = reinterpret_cast<unsigned *>(k2_smem);
+    sc.colw = sc.flw + k2_bits_words();
+    sc.cnt = reinterpret_cast<int *>(sc.colw + k2_bits_words());
+    sc.off = sc.cnt + 2 * K2_MAXN + 8;
     __shared__ int s_bad;
     if (tid == 0) s_bad = 0;
     __syncthreads();
-    for (int i = tid; i < N; i += blockDim.x) {
-        uint8_t v = mask_in[i];
+    for (int pw = warp; pw < n * 4; pw += K2_THREADS / 32) {
+        const int r = pw >> 2, c = (pw & 3) * 32 + lane;
+        const uint8_t v = c < n ? mask_in[r * n + c] : 0;
         if (v > 1) s_bad = 1;
-        s_fl[i] = v ? 1 : 0;
+        const unsigned b = __ballot_sync(0xffffffffu, v != 0);
+        if (lane == 0) sc.flw[pw] = b;
     }
     __syncthreads();
     if (s_bad) {
         if (tid == 0) { *a.nnzb = -1; if (a.flags) atomicOr(a.flags, FLAG_BAD_MASK); }
         return;
     }
-    build_bsr_and_plan(s_fl, n, a.block, a.brow_ptr, a.bcol_idx, a.bcol_ptr, a.brow_idx, a.mask, a.nnzb,
-                       a.nnzb_cap, a.plan, a.flags, s_cnt, s_off);
+    build_bsr_and_plan(a, sc);
 }
 
 // ---------------------------------------------------------------- host side
+unsigned long long *g_k2_trace = nullptr;
 size_t pattern_ws_bytes(int L, int block) {
     const int n = L / block;
     return 256 + round_up((size_t)n * n * 8, 256);
 }
 
 static size_t k2_smem_bytes(int n, bool with_pool) {
-    const size_t N = (size_t)n * n;
-    const size_t N16 = round_up(N, 16);
-    size_t b = with_pool ? N * 8 + 2 * N16 : N16;
-    b += (2 * n + 8) * 4 + (2 * (n + 1) + 8) * 4 + 256 * 4 + 64;
+    size_t b = with_pool ? (((size_t)n * n + 1) & ~(size_t)1) * 8 + 4 * (size_t)k2_bits_words() * 4 : 0;  // pool, gt/dn/rt/dg
+    b += 2 * (size_t)k2_bits_words() * 4;                                             // fl, columns
+    b += (2 * K2_MAXN + 8) * 4 + (2 * (K2_MAXN + 1) + 8) * 4 + 256 * 4 + 64;
     return b;
 }
 
 spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos,
                             long long T_abs, void *ws, spion_bsr *out, cudaStream_t s) {
     const int n = L / B;
+    if (n > K2_MAXN) return SPION_ERR_UNSUPPORTED;
     int *flags = reinterpret_cast<int *>(ws);
     unsigned long long *pool = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + 256);
     SPION_CUDA_TRY(cudaMemsetAsync(ws, 0, 256 + (size_t)n * n * 8, s));
@@ -466,6 +576,7 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     SPION_LAUNCH_CHECK();
 
     K2Args a;
+    memset(&a, 0, sizeof(a));
     a.pool = reinterpret_cast<const long long *>(pool);
     a.n = n;
     a.block = B;
@@ -482,13 +593,19 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     a.mask = out->mask;
     a.nnzb_cap = out->nnzb_cap;
     a.plan = reinterpret_cast<int *>(out->plan);
+    if (getenv("SPION_TRACE")) {
+        static unsigned long long *tb = nullptr;
+        if (!tb) SPION_CUDA_TRY(cudaMalloc(&tb, 64 * 8));
+        a.trace = tb;
+        g_k2_trace = tb;
+    }
     const size_t smem2 = k2_smem_bytes(n, true);
+    if (smem2 > 227 * 1024) return SPION_ERR_UNSUPPORTED;
     static bool attr2 = false;
     if (!attr2) {
         SPION_CUDA_TRY(allow_max_dyn_smem(pattern_finalize_kernel));
         attr2 = true;
     }
-    if (smem2 > 227 * 1024) return SPION_ERR_UNSUPPORTED;
     pattern_finalize_kernel<<<1, K2_THREADS, smem2, s>>>(a);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
@@ -496,6 +613,7 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
 
 spion_status launch_bsr_from_mask(const uint8_t *mask, int L, int B, spion_bsr *out, int *flags, cudaStream_t s) {
     const int n = L / B;
+    if (n > K2_MAXN) return SPION_ERR_UNSUPPORTED;
     K2Args a;
     memset(&a, 0, sizeof(a));
     a.n = n;

@@ -1,0 +1,25 @@
+"""Debug: K2 phase timestamps (SPION_TRACE=1) and K1/K2 durations for each LRA shape."""
+import ctypes, os, sys
+os.environ["SPION_TRACE"] = "1"
+import numpy as np, torch
+sys.path.insert(0, ".")
+import synth
+from paper_2309_12578_b200 import spion, _native as N
+lib = N.lib()
+lib.spion_debug_k2_trace.restype = ctypes.c_int64
+for L, B in [(1024, 32), (2048, 64), (4096, 64)]:
+    A = synth.syn_scores(L, B, heads=2, seed=1, device="cuda")
+    bp = spion.pattern(A, B, filter=31, alpha=75.0, sync=True)
+    for _ in range(3):
+        spion.pattern(A, B, filter=31, alpha=75.0, out=bp, sync=True)
+    buf = (ctypes.c_ulonglong * 8)()
+    lib.spion_debug_k2_trace(buf)
+    t = np.array(buf[:7], dtype=np.int64)
+    d = np.diff(t) / 1000
+    print(L, B, "K2 phases us: load %.2f thresh %.2f edges %.2f flood %.2f fl %.2f bsr+plan %.2f total %.2f" % (*d, (t[6] - t[0]) / 1000))
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(20):
+        spion.pattern(A, B, filter=31, alpha=75.0, out=bp)
+    e1.record(); torch.cuda.synchronize()
+    print("   pattern call avg us", e0.elapsed_time(e1) / 20 * 1000)
