@@ -24,51 +24,72 @@ namespace spion {
 
 // ---------------------------------------------------------------- K1
 static constexpr int K1_WARPS = 8;
-static constexpr int K1_MAXP = 4;   // (target row, column) pairs per lane
-static constexpr int K1_PREF = 6;   // float4 loads per lane kept in flight (covers W <= 768)
+static constexpr int K1_MAXP = 2;  // (target row, column) pairs per lane
 
 struct K1Geom {
-    int L, B, h, A, nI, JC, n_cc, W, CH;
+    int L, B, h, A, nI, JC, n_cc, RP;  // RP: source rows per CTA (grid.z splits the B rows)
 };
 
-static K1Geom k1_geom(int L, int B, int F) {
-    K1Geom g;
+// Window of one CTA: positions [g4, g4 + 128*K4) of a source row (float4-aligned, g4 <= c0);
+// lane l owns positions [4*K4*l, 4*K4*(l+1)).
+static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
     g.L = L;
     g.B = B;
     g.h = (F - 1) / 2;
     g.A = (g.h + B - 1) / B;
     g.nI = 2 * g.A + 1;
-    int n = L / B;
-    int jc = 8;
-    while (jc > 1 && g.nI * jc > 32 * K1_MAXP) --jc;
-    if (jc > n) jc = n;
-    g.JC = jc;
-    g.n_cc = (n + jc - 1) / jc;
-    g.W = jc * B + 2 * g.h;
-    int ch = (g.W + 2 + 31) / 32;
-    if ((ch & 1) == 0) ++ch;  // odd chunk -> conflict-free strided smem access
-    g.CH = ch;
-    return g;
+    const int n = L / B;
+    // positions used: [0, W + o] with W = JC*B + 2h, o <= 3
+    int jmax = (128 * K4 - 2 * g.h - 4) / B;
+    jmax = min(jmax, 32 * K1_MAXP / g.nI);
+    if (jmax < 1) return false;
+    const int n_cc = (n + jmax - 1) / jmax;
+    g.JC = (n + n_cc - 1) / n_cc;
+    g.n_cc = (n + g.JC - 1) / g.JC;
+    int rs = 1;  // split the rows of a block row until the grid covers the GPU a few times
+    while (g.n_cc * n * rs < 4 * 148 && B / (2 * rs) >= 2 * K1_WARPS) rs *= 2;
+    g.RP = (B + rs - 1) / rs;
+    return true;
 }
 
+template <int K4>
+struct K1Cfg {
+    static constexpr int CH = 4 * K4;                    // positions per lane
+    static constexpr bool POW2 = (K4 & (K4 - 1)) == 0;
+    static constexpr int LOGK4 = K4 == 2 ? 1 : K4 == 4 ? 2 : K4 == 8 ? 3 : 0;
+    static constexpr bool HOLD = K4 <= 8;                // lane's q in registers, next row prefetched
+    // staging (float4): v at v + v/K4 when K4 is even (an odd lane stride keeps the LDS.128 of a
+    // lane's own chunk conflict-free); PP (u64): element-major, lane-minor (conflict-free STS.64)
+    static constexpr int STAGE4 = POW2 ? 32 * (K4 + 1) : 32 * K4;
+    static constexpr size_t WARP_BYTES = (size_t)STAGE4 * 16 + (size_t)32 * CH * 8;
+    static __device__ __forceinline__ int sidx(int v) { return POW2 ? v + (v >> LOGK4) : v; }
+    static __device__ __forceinline__ int own4(int lane, int i) { return POW2 ? lane * (K4 + 1) + i : lane * K4 + i; }
+    static __device__ __forceinline__ int ppidx(int pos) { return (pos % CH) * 32 + pos / CH; }
+};
+
+template <int K4>
 __global__ void __launch_bounds__(K1_WARPS * 32)
 pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *__restrict__ pool,
                     int *__restrict__ flags) {
+    using C = K1Cfg<K4>;
+    constexpr int CH = C::CH;
     extern __shared__ __align__(16) unsigned char k1_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = g.L, B = g.B, h = g.h, n = L / B;
     const int cc = blockIdx.x, I0 = blockIdx.y;
     const int J0 = cc * g.JC;
     const int ncols = min(g.JC, n - J0);
-    const int W = ncols * B + 2 * h;  // columns [c0, c0 + W)
+    const int W = ncols * B + 2 * h;  // window-relative columns k in [0, W], column = c0 + k
     const int c0 = J0 * B - h;
-    const int CH = g.CH;
-    const int ROW = 32 * CH;
-    unsigned long long *rowq = reinterpret_cast<unsigned long long *>(k1_smem) + (size_t)warp * ROW;
-    unsigned long long *s_acc = reinterpret_cast<unsigned long long *>(k1_smem) + (size_t)K1_WARPS * ROW;
+    const int g4 = (c0 >= 0) ? (c0 & ~3) : -((-c0 + 3) & ~3);
+    const int o = c0 - g4;            // position = k + o
+    const int n4 = (W + o + 1 + 3) >> 2;
+    unsigned char *wbase = k1_smem + (size_t)warp * C::WARP_BYTES;
+    float4 *stage = reinterpret_cast<float4 *>(wbase);
+    unsigned long long *pp = reinterpret_cast<unsigned long long *>(wbase + (size_t)C::STAGE4 * 16);
+    unsigned long long *s_acc = reinterpret_cast<unsigned long long *>(k1_smem + (size_t)K1_WARPS * C::WARP_BYTES);
     const int npairs = g.nI * ncols;
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) s_acc[p] = 0ull;
-    for (int k = W + lane; k < ROW; k += 32) rowq[k] = 0ull;  // beyond the window: zero once
 
     // loop-invariant (target row offset a, column jj) pairs of this lane
     int pa[K1_MAXP], pj[K1_MAXP];
@@ -80,71 +101,104 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
         pj[t] = p < npairs ? p % ncols : 0;
         acc[t] = 0ull;
     }
+    // which of this lane's float4 loads hit [0, L) (the same for every row): zero padding elsewhere
+    unsigned vmask = 0;
+#pragma unroll
+    for (int i = 0; i < K4; ++i) {
+        const int v = lane + 32 * i;
+        const int gc = g4 + 4 * v;
+        if (v < n4 && gc >= 0 && gc < L) vmask |= 1u << i;
+    }
+    const int colbase = g4 + 4 * lane;
     bool bad = false;
-
-    // float4 window covering [c0, c0+W)
-    const int g4 = (c0 >= 0) ? (c0 & ~3) : -((-c0 + 3) & ~3);
-    const int n4 = (c0 + W - g4 + 3) >> 2;
+    const int u_begin = blockIdx.z * g.RP, u_end = min(B, u_begin + g.RP);
     __syncthreads();
 
-    auto load4 = [&](const float *arow, int v) -> float4 {
-        const int gc = g4 + 4 * v;
-        return (v < n4 && gc >= 0 && gc < L) ? __ldg(reinterpret_cast<const float4 *>(arow + gc))
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-    };
-    // q (int64 fixed point, reading Q8) of one float4 into the row buffer; zero outside [0, L)
-    auto stage4 = [&](float4 f, int v) {
-        if (v >= n4) return;
-        const int gc = g4 + 4 * v;
-        const float av[4] = {f.x, f.y, f.z, f.w};
+    auto load_row = [&](int u, float4 (&dst)[K4]) {
+        const float *arow = A + (size_t)(I0 * B + u) * L + colbase;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int k = gc + t - c0;
-            if (k < 0 || k >= W) continue;
-            const float a = av[t];
-            if (!(a >= 0.f && a <= 1.f)) bad = true;
-            // a * 2^32 is exact in fp32; round half to even
-            rowq[k] = (unsigned long long)__float2ll_rn(a * 4294967296.0f);
-        }
+        for (int i = 0; i < K4; ++i)
+            dst[i] = ((vmask >> i) & 1u) ? __ldg(reinterpret_cast<const float4 *>(arow + 128 * i))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
     };
+    // q = rint(a * 2^32) (reading Q8; a * 2^32 is exact in fp32, round half to even).  For a in
+    // [0, 1) q < 2^32 is the u32 conversion; a = 1 saturates it to 2^32 - 1 and is fixed up below.
+    auto lo32 = [](float a) -> unsigned { return __float2uint_rn(a * 4294967296.0f); };
+    auto elem = [](const float4 &f, int t) -> float { return t == 0 ? f.x : t == 1 ? f.y : t == 2 ? f.z : f.w; };
 
-    float4 cur[K1_PREF];
-    if (warp < B) {
-        const float *arow = A + (size_t)(I0 * B + warp) * L;
+    float4 cur[K4];
+    int u = u_begin + warp;
+    if (C::HOLD && u < u_end) load_row(u, cur);
+    for (; u < u_end; u += K1_WARPS) {
+        if (!C::HOLD) load_row(u, cur);
 #pragma unroll
-        for (int i = 0; i < K1_PREF; ++i) cur[i] = load4(arow, lane + 32 * i);
-    }
-    for (int u = warp; u < B; u += K1_WARPS) {
-        const float *arow = A + (size_t)(I0 * B + u) * L;
-#pragma unroll
-        for (int i = 0; i < K1_PREF; ++i) stage4(cur[i], lane + 32 * i);
-        for (int v = lane + 32 * K1_PREF; v < n4; v += 32) stage4(load4(arow, v), v);  // wide windows
-        if (u + K1_WARPS < B) {  // next row in flight during the scans below
-            const float *nrow = arow + (size_t)K1_WARPS * L;
-#pragma unroll
-            for (int i = 0; i < K1_PREF; ++i) cur[i] = load4(nrow, lane + 32 * i);
-        }
+        for (int i = 0; i < K4; ++i) stage[C::sidx(lane + 32 * i)] = cur[i];
         __syncwarp();
-        // chunk totals of q and of sum_t q_t (CH-1-t), the chunk's contribution to the P sum
-        const int k0 = lane * CH;
-        unsigned long long tot = 0, wsum = 0;
-        for (int t = 0; t < CH; ++t) {
-            const unsigned long long qv = rowq[k0 + t];
-            tot += qv;
-            wsum += qv * (unsigned long long)(CH - 1 - t);
+        if (C::HOLD && u + K1_WARPS < u_end) load_row(u + K1_WARPS, cur);  // next row in flight
+
+        // pass 1 over the lane chunk: tot = sum q, ppl = sum_e q_e (CH-1-e) (the chunk's P-sum share)
+        unsigned lo[C::HOLD ? CH : 1];
+        unsigned long long tot = 0, ppl = 0;
+        bool fast = true;  // every element in [0, 1)
+#pragma unroll
+        for (int i = 0; i < K4; ++i) {
+            const float4 f = stage[C::own4(lane, i)];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float a = elem(f, t);
+                fast = fast && (a >= 0.f) && (a < 1.f);
+                const unsigned l = lo32(a);
+                if constexpr (C::HOLD) lo[4 * i + t] = l;
+                tot += l;
+                ppl += (unsigned long long)l * (unsigned)(CH - 1 - (4 * i + t));
+            }
         }
-        // P[k] = sum_{c<k} q[c] (P at chunk start: off1); PP[k] = sum_{k'<k} P[k'] (in place)
+        const bool slow = !__all_sync(0xffffffffu, fast);
+        unsigned fix = 0;  // HOLD: bit e set where q_e = 2^32 (a = 1): one more than the saturated u32
+        if (slow) {
+#pragma unroll
+            for (int i = 0; i < K4; ++i) {
+                const float4 f = stage[C::own4(lane, i)];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float a = elem(f, t);
+                    if (!(a >= 0.f && a <= 1.f)) bad = true;
+                    if (a >= 1.f) {
+                        const int e = 4 * i + t;
+                        if constexpr (C::HOLD) fix |= 1u << e;
+                        tot += 1;
+                        ppl += (unsigned long long)(CH - 1 - e);
+                    }
+                }
+            }
+        }
+        // P at the chunk start (off1) and PP at the chunk start (off2); PP of every position
         const unsigned long long off1 = warp_excl_scan_u64(tot, lane);
-        const unsigned long long off2 = warp_excl_scan_u64((unsigned long long)CH * off1 + wsum, lane);
+        const unsigned long long off2 = warp_excl_scan_u64((unsigned long long)CH * off1 + ppl, lane);
         unsigned long long run = off1, run2 = off2;
-        for (int t = 0; t < CH; ++t) {
-            const unsigned long long qv = rowq[k0 + t];
-            rowq[k0 + t] = run2;
-            run2 += run;
-            run += qv;
+#pragma unroll
+        for (int i = 0; i < K4; ++i) {
+            float4 f;
+            if constexpr (!C::HOLD) f = stage[C::own4(lane, i)];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int e = 4 * i + t;
+                unsigned long long qv;
+                if constexpr (C::HOLD) {
+                    qv = (unsigned long long)lo[e] + ((fix >> e) & 1u);
+                } else {
+                    const float a = elem(f, t);
+                    qv = (unsigned long long)lo32(a) + (a >= 1.f ? 1u : 0u);
+                }
+                pp[e * 32 + lane] = run2;
+                run2 += run;
+                run += qv;
+            }
         }
         __syncwarp();
-        // contributions of row x = I0*B+u to pool rows I0+a, columns J0+jj
+        // contributions of source row x = I0*B + u to pool rows I0+a, columns J0+jj:
+        //   sum_{f in F} Wrow(x, (J0+jj)*B + f) = (PP[s1+1+B] - PP[s0+B]) - (PP[s1+1] - PP[s0])
+        auto PP = [&](int k) -> unsigned long long { return pp[C::ppidx(k + o)]; };
 #pragma unroll
         for (int t = 0; t < K1_MAXP; ++t) {
             const int a = pa[t];
@@ -154,7 +208,7 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
             const int f0 = max(r - B + 1, -h), f1 = min(r, h);
             if (f0 > f1) continue;
             const int s0 = pj[t] * B + h + f0, s1 = pj[t] * B + h + f1;
-            acc[t] += (rowq[s1 + 1 + B] - rowq[s0 + B]) - (rowq[s1 + 1] - rowq[s0]);
+            acc[t] += (PP(s1 + 1 + B) - PP(s0 + B)) - (PP(s1 + 1) - PP(s0));
         }
         __syncwarp();
     }
@@ -171,6 +225,26 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
         if (I < 0 || I >= n || s_acc[p] == 0ull) continue;
         atomicAdd(&pool[(size_t)I * n + (J0 + jj)], s_acc[p]);
     }
+}
+
+template <int K4>
+static size_t k1_smem_bytes(const K1Geom &g) {
+    return (size_t)K1_WARPS * K1Cfg<K4>::WARP_BYTES + (size_t)g.nI * g.JC * 8;
+}
+
+template <int K4>
+static spion_status k1_launch(const float *scores, const K1Geom &g, unsigned long long *pool, int *flags,
+                              cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        SPION_CUDA_TRY(allow_max_dyn_smem(pattern_pool_kernel<K4>));
+        attr = true;
+    }
+    const int n = g.L / g.B;
+    const int rs = (g.B + g.RP - 1) / g.RP;
+    pattern_pool_kernel<K4><<<dim3(g.n_cc, n, rs), K1_WARPS * 32, k1_smem_bytes<K4>(g), s>>>(scores, g, pool, flags);
+    SPION_LAUNCH_CHECK();
+    return SPION_OK;
 }
 
 // ---------------------------------------------------------------- K2
@@ -564,16 +638,15 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     int *flags = reinterpret_cast<int *>(ws);
     unsigned long long *pool = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + 256);
     SPION_CUDA_TRY(cudaMemsetAsync(ws, 0, 256 + (size_t)n * n * 8, s));
-    K1Geom g = k1_geom(L, B, F);
-    const size_t smem1 = ((size_t)K1_WARPS * 32 * g.CH + (size_t)g.nI * g.JC) * 8;
-    if (smem1 > 200 * 1024) return SPION_ERR_UNSUPPORTED;
-    static bool attr1 = false;
-    if (!attr1) {
-        SPION_CUDA_TRY(allow_max_dyn_smem(pattern_pool_kernel));
-        attr1 = true;
-    }
-    pattern_pool_kernel<<<dim3(g.n_cc, n), K1_WARPS * 32, smem1, s>>>(scores, g, pool, flags);
-    SPION_LAUNCH_CHECK();
+    K1Geom g4, g8, g;
+    spion_status st;
+    const bool ok4 = k1_geom(L, B, F, 4, g4), ok8 = k1_geom(L, B, F, 8, g8);
+    // fewest window positions per source row (ties: the 16-position lanes, more CTAs)
+    if (ok4 && (!ok8 || g4.n_cc * 4 <= g8.n_cc * 8)) st = k1_launch<4>(scores, g4, pool, flags, s);
+    else if (ok8) st = k1_launch<8>(scores, g8, pool, flags, s);
+    else if (k1_geom(L, B, F, 17, g)) st = k1_launch<17>(scores, g, pool, flags, s);
+    else return SPION_ERR_UNSUPPORTED;  // B + F > ~2170 columns per window
+    if (st != SPION_OK) return st;
 
     K2Args a;
     memset(&a, 0, sizeof(a));

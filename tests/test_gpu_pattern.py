@@ -52,6 +52,9 @@ CASES = [
     (64, 64, 31, 50.0, "linear"),        # nblk = 1
     (96, 4, 63, 60.0, "linear"),         # h > B (targets span several pool rows)
     (1024, 32, 31, 0.05, "absolute"),
+    (1024, 64, 601, 70.0, "linear"),     # wide filter: window > 636 columns (17-float4 lanes)
+    (2048, 1024, 31, 50.0, "linear"),    # block wider than the small window
+    (1280, 10, 31, 75.0, "linear"),      # B not a multiple of 4 (windows start mid-float4)
 ]
 
 
