@@ -135,7 +135,8 @@ SPION_API spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, i
                                  int32_t *nnzb_host, void *stream);
 
 /* Bytes of device workspace spion_attn_bwd needs: D_i = rowsum(dO*O), fp32
- * [bh][L] (the backward is atomic-free and deterministic).  spion_attn_fwd
+ * [bh][L], and -lse_i*log2(e), fp32 [bh][L] (written by the dQ pass for the
+ * dK/dV pass; the backward is atomic-free and deterministic).  spion_attn_fwd
  * needs none. */
 SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt);
 

@@ -177,7 +177,8 @@ spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t blo
 size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt) {
     (void)dt;
     if (bh <= 0 || L <= 0 || d <= 0) return 0;
-    return round_up((size_t)bh * L * 4, 256);  // D_i = rowsum(dO * O), fp32
+    // D_i = rowsum(dO * O) and -lse_i * log2(e) (the dK/dV kernel's exponent offset), fp32
+    return round_up((size_t)bh * L * 4, 256) * 2;
 }
 
 static spion_status check_attn_common(const void *Q, const void *K, const void *V, int64_t bh, int32_t L,
@@ -260,6 +261,7 @@ spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_
     a.dV = dV_dev;
     float *D = static_cast<float *>(ws_dev);
     a.D = D;
+    a.nlse2 = reinterpret_cast<float *>(static_cast<char *>(ws_dev) + round_up((size_t)bh * L * 4, 256));
     if (dt == SPION_BF16 && tc_supported(a, dt)) return launch_bwd_tc(a, s);
     if (!simt_supported(a.B, d)) return SPION_ERR_UNSUPPORTED;
     st = launch_bwd_preprocess(a, dt, D, s);

@@ -9,6 +9,7 @@ struct AttnArgs {
     void *Oout, *dQ, *dK, *dV;
     float *lse_out;
     const float *lse, *D;
+    float *nlse2;  // bwd workspace: -lse * log2(e), written by the dQ pass (tensor-core path)
     int64_t bh, stride_bh, stride_l;
     int L, d, B, n;
     int mode;

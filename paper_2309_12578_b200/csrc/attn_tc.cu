@@ -70,6 +70,7 @@ struct TcParams {
     float *lse_out;       // fwd out
     const float *lse;     // bwd in
     float *D;             // dq out, dkdv in
+    float *nlse2;         // dq out: -lse * log2(e) (the dK/dV pass stages it instead of lse)
     void *dQ, *dK, *dV;   // bwd out (bf16)
     const int *plan;
     const int *brow_ptr;
@@ -105,8 +106,10 @@ struct Tracer {
     }
 };
 
+// offset arithmetic on the __shared__ array (not an integer round trip), so the
+// compiler keeps the shared address space and emits LDS/STS for the staged tiles
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
-    return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+    return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
 // ---------------------------------------------------------------- dynamic tile scheduler
@@ -376,29 +379,30 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 float alpha = 1.f;
                 bool rescale = false;
                 if (active) {
-                    float s[B];
+                    float s[B];  // raw scores; the softmax scale is folded into the exponent
 #pragma unroll
                     for (int hh = 0; hh < B / 32; ++hh) {
                         float v[32];
                         tmem_ld32(tl + sb * B + hh * 32, v);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) s[hh * 32 + i] = v[i] * sl2;
+                        for (int i = 0; i < 32; ++i) s[hh * 32 + i] = v[i];
                     }
                     float mx = s[0];
 #pragma unroll
                     for (int i = 1; i < B; ++i) mx = fmaxf(mx, s[i]);
+                    mx *= sl2;  // scale > 0: max commutes with the scaling (log2 domain)
                     if (m_run == -INFINITY) {
                         m_run = mx;
                     } else if (mx > m_run + 8.f) {  // rescale only on a large max increase
-                        alpha = exp2f(m_run - mx);
+                        alpha = ex2(m_run - mx);
                         m_run = mx;
                         rescale = true;
                     }
                     float sum = 0.f;
 #pragma unroll
                     for (int i = 0; i < B; i += 2) {
-                        const float e0 = exp2f(s[i] - m_run), e1 = exp2f(s[i + 1] - m_run);
+                        const float e0 = ex2(fmaf(s[i], sl2, -m_run)), e1 = ex2(fmaf(s[i + 1], sl2, -m_run));
                         sum += e0 + e1;
                         packed[i / 2] = pack_bf16(e0, e1);
                     }
@@ -648,7 +652,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 continue;
             }
             const int qb = nq & 1;
-            const float lse2 = valid ? p.lse[(int64_t)bh * p.L + row] * LOG2E : 0.f;
+            const float nl2 = valid ? -p.lse[(int64_t)bh * p.L + row] * LOG2E : 0.f;
             // D_i = dO_i . O_i from the staged (swizzled) tiles
             mbar_wait(q_full + qb, (nq >> 1) & 1);
             mbar_wait(o_full, nq & 1);
@@ -670,7 +674,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 }
             }
             mbar_arrive(o_empty);
-            if (valid) p.D[(int64_t)bh * p.L + row] = Dr;
+            if (valid) {
+                p.D[(int64_t)bh * p.L + row] = Dr;
+                p.nlse2[(int64_t)bh * p.L + row] = nl2;
+            }
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;
                 const uint32_t gs = g + jj, sb = gs % NBUF;
@@ -687,8 +694,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
-                            const float p0 = exp2f(fmaf(sv[i], sl2, -lse2));
-                            const float p1 = exp2f(fmaf(sv[i + 1], sl2, -lse2));
+                            const float p0 = ex2(fmaf(sv[i], sl2, nl2));
+                            const float p1 = ex2(fmaf(sv[i + 1], sl2, nl2));
                             pk[i / 2] = pack_bf16(p0 * (dp[i] - Dr), p1 * (dp[i + 1] - Dr));
                         }
                     } else {
@@ -897,8 +904,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             for (int jj = 0; jj < cnt; ++jj) {
                 const bool active = (msks[jj] >> slot) & 1;
                 mbar_wait(q_full + st, ph);  // lse_I, D_I
-                const float *slse = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
-                const float *sD = slse + 128;
+                const float *snl2 = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
+                const float *sD = snl2 + 128;
                 const uint32_t gs = g + jj, sb = gs % NBUF;
                 mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dV/dK MMAs that read sb before
                 tc_fence_after();
@@ -907,17 +914,23 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 for (int hh = 0; hh < B / 32; ++hh) {
                     uint32_t pk[16], dk[16];
                     if (active) {
-                        float sv[32], dp[32];
+                        float sv[32], dp[32], nl[32], dd[32];
                         tmem_ld32(tl + cs + hh * 32, sv);
                         tmem_ld32(tl + cs + B + hh * 32, dp);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {  // broadcast LDS.128 of the query block's offsets
+                            const float4 a = reinterpret_cast<const float4 *>(snl2 + hh * 32)[i];
+                            const float4 b = reinterpret_cast<const float4 *>(sD + hh * 32)[i];
+                            nl[4 * i] = a.x; nl[4 * i + 1] = a.y; nl[4 * i + 2] = a.z; nl[4 * i + 3] = a.w;
+                            dd[4 * i] = b.x; dd[4 * i + 1] = b.y; dd[4 * i + 2] = b.z; dd[4 * i + 3] = b.w;
+                        }
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
-                            const int q = hh * 32 + i;
-                            const float p0 = exp2f(fmaf(sv[i], sl2, -slse[q] * LOG2E));
-                            const float p1 = exp2f(fmaf(sv[i + 1], sl2, -slse[q + 1] * LOG2E));
+                            const float p0 = ex2(fmaf(sv[i], sl2, nl[i]));
+                            const float p1 = ex2(fmaf(sv[i + 1], sl2, nl[i + 1]));
                             pk[i / 2] = pack_bf16(p0, p1);
-                            dk[i / 2] = pack_bf16(p0 * (dp[i] - sD[q]), p1 * (dp[i + 1] - sD[q + 1]));
+                            dk[i / 2] = pack_bf16(p0 * (dp[i] - dd[i]), p1 * (dp[i + 1] - dd[i + 1]));
                         }
                     } else {
 #pragma unroll
@@ -1102,12 +1115,13 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     p.O = const_cast<void *>(a.O);
     p.lse = a.lse;
     p.D = const_cast<float *>(a.D);
+    p.nlse2 = a.nlse2;
     p.dQ = a.dQ;
     attn_bwd_dq_tc_kernel<B><<<grid_for(p, Cfg<B>::DQ_CTAS), TC_THREADS, dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, p);
     SPION_LAUNCH_CHECK();
     // 2) dK, dV (column tiles)
     TcParams q = base_params(a, 2, Cfg<B>::DKV_CTAS);
-    q.lse = a.lse;
+    q.lse = a.nlse2;  // staged per query block: -lse * log2(e)
     q.D = const_cast<float *>(a.D);
     q.dK = a.dK;
     q.dV = a.dV;
