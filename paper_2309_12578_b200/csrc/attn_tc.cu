@@ -21,9 +21,13 @@
 //   for I:  S^T = K Q_I^T, dP^T = V dO_I^T -> P^T, dS^T (TMEM)
 //           -> dV += P^T dO_I, dK += dS^T Q_I (TMEM);  dK * scale -> bf16.
 //
-// Warp roles (192 threads): warps 0-3 softmax / epilogue (thread = TMEM lane =
-// tile row), warp 4 scheduler + TMA producer, warp 5 MMA issuer (one elected
-// lane of a converged warp) and TMEM allocator.  One CTA per SM owns all 512 TMEM
+// Warp roles: warps 0..MW-1 softmax / epilogue (thread = TMEM lane = tile row;
+// with MW = 8 the two warpgroups take the two column halves of every block),
+// warp MW scheduler + TMA producer, warp MW+1 MMA issuer (one elected lane of a
+// converged warp) and TMEM allocator.  The forward has MW = 4; the backward
+// kernels MW = 8 where one CTA owns the SM.  A softmax warp writes its packed bf16
+// P / dS over the first half of each 32-column chunk it has read itself, so the
+// two warpgroups never race on TMEM columns.  One CTA per SM owns all 512 TMEM
 // columns: S (and dP) rotate through NBUF buffers so the MMA warp runs up to NBUF
 // blocks ahead of the softmax warps; P / dS are written back
 // into TMEM as packed bf16 and consumed as the A operand of the next MMA
@@ -43,7 +47,9 @@ namespace spion {
 
 using namespace tc;
 
-static constexpr int TC_THREADS = 192;
+static constexpr int TC_THREADS = 224;  // forward: 4 softmax warps + producer + MMA + storer
+// backward: MW softmax warps, then the producer, MMA and storer warps
+__host__ __device__ constexpr int bwd_threads(int mw) { return 32 * (mw + 3); }
 // Per-kernel, per-B configuration.  CTAS CTAs per SM share the 512 TMEM columns
 // (COLS each) and ~227 KB of shared memory; NBUF score buffers let the MMA warp run
 // up to NBUF blocks ahead of the softmax warps; TMA rings have NST >= NBUF stages
@@ -59,6 +65,9 @@ template <int B> struct Cfg {
     static constexpr int DKV_CTAS = B == 32 ? 2 : 1, DKV_COLS = 512 / DKV_CTAS;
     static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
     static constexpr int DKV_NST = B == 32 ? 4 : 9;              // Q_I + dO_I + lse_I + D_I per stage
+    // softmax warps of the backward kernels: two warpgroups (each takes half of a block's
+    // columns) where one CTA owns the SM, one warpgroup where two CTAs share it
+    static constexpr int DQ_MW = DQ_CTAS == 1 ? 8 : 4, DKV_MW = DKV_CTAS == 1 ? 8 : 4;
     static_assert(FWD_NST >= FWD_NBUF && DQ_NST >= DQ_NBUF && DKV_NST >= DKV_NBUF, "ring shallower than look-ahead");
 };
 static constexpr int SCHED_CAP = 128;  // max entries of one tile list (nblk <= 128)
@@ -137,10 +146,11 @@ __device__ __forceinline__ Sched make_sched(uint8_t *area, uint64_t *bars) {
     return s;
 }
 
-__device__ __forceinline__ void sched_init(const Sched &sc) {
+// `consumers` warps release each slot: the MMA warp and every softmax warp
+__device__ __forceinline__ void sched_init(const Sched &sc, int consumers = 5) {
     for (int i = 0; i < 4; ++i) {
         mbar_init(sc.full + i, 1);
-        mbar_init(sc.empty + i, 5);
+        mbar_init(sc.empty + i, consumers);
     }
 }
 
@@ -216,6 +226,17 @@ __device__ __forceinline__ void store_row_bf16(__nv_bfloat16 *dst, const float (
     }
 }
 
+// row r, columns [32 half, 32 half + 32) of a [128][64] bf16 SW128 K-major tile in shared
+// memory (the TMA box layout): 16-byte chunks at their swizzled place, conflict-free
+__device__ __forceinline__ void stage_row_bf16(uint8_t *tile, int r, const float (&v)[32], float f, int half) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        *reinterpret_cast<uint4 *>(tile + sw128_offset(r, half * 4 + c)) =
+            make_uint4(pack_bf16(v[8 * c] * f, v[8 * c + 1] * f), pack_bf16(v[8 * c + 2] * f, v[8 * c + 3] * f),
+                       pack_bf16(v[8 * c + 4] * f, v[8 * c + 5] * f), pack_bf16(v[8 * c + 6] * f, v[8 * c + 7] * f));
+    }
+}
+
 __device__ __forceinline__ void zero_row_bf16(__nv_bfloat16 *dst) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) reinterpret_cast<uint4 *>(dst)[c] = make_uint4(0, 0, 0, 0);
@@ -230,12 +251,13 @@ __device__ __forceinline__ void zero_row_bf16(__nv_bfloat16 *dst) {
 template <int B>
 __global__ void __launch_bounds__(TC_THREADS, Cfg<B>::FWD_CTAS)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, TcParams p) {
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, TcParams p) {
     constexpr int NST = Cfg<B>::FWD_NST, NBUF = Cfg<B>::FWD_NBUF;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;  // stage: K at +0, V at +KV_BYTES
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, 64, false, true);
     constexpr uint32_t COL_O = NBUF * B;  // S / P buffer b at columns [B b, B b + B)
+    constexpr int W_PROD = 4, W_MMA = 5, W_STORE = 6;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
@@ -250,25 +272,29 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
              *freeb = p_full + NBUF, *kv_full = freeb + NBUF, *kv_empty = kv_full + NST;
     Sched sc = make_sched(sSched, kv_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
+    uint64_t *staged = kv_empty + NST + 9;  // [2]: O of the item using Q buffer qb staged
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
+        // q_empty: the last S of the item, and the epilogue's TMA store of O (staged in the
+        // same buffer) having read shared memory
+        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 2); }
         for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); mbar_init(freeb + i, 1); }
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
-        sched_init(sc);
+        for (int i = 0; i < 2; ++i) mbar_init(staged + i, 128);
+        sched_init(sc, 6);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<Cfg<B>::FWD_COLS>(tmem_slot);
+    if (warp == W_MMA) tmem_alloc<Cfg<B>::FWD_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int nitems = (int)(p.bh * p.ntiles);
 
-    if (warp == 4) {
+    if (warp == W_PROD) {
         // ------------------------------------------------------------ scheduler + TMA producer
-        if (lane == 0) { prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV); }
+        if (lane == 0) { prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmO); }
         int st = 0, nq = 0;
         uint32_t ph = 0;
         for (int ks = 0;; ++ks) {
@@ -299,7 +325,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             }
             __syncwarp();
         }
-    } else if (warp == 5) {
+    } else if (warp == W_MMA) {
         // ------------------------------------------------------------ MMA issuer (converged warp,
         // one elected lane issues): S for up to NBUF blocks ahead, then P.V as P arrives
         int sst = 0, pst = 0, nq = 0;  // ring cursors of the next S and the next P.V
@@ -353,12 +379,36 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             }
             sched_release(sc, ks, true);
         }
+    } else if (warp == W_STORE) {
+        // storer: once the softmax warps have staged an item's output tile(s) in shared
+        // memory, one TMA store per tile; the buffer is released when the store has read it
+        int ns = 0;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int bh = h[1], t = h[2], cnt = h[3];
+            if (cnt > 0) {
+                const int sb = ns & 1;
+                mbar_wait(staged + sb, (ns >> 1) & 1);
+                ++ns;
+                if (lane == 0) {
+                    tma_store_3d(&tmO, sQ + sb * 16384, 0, t * 128, bh);
+                    bulk_commit();
+                    bulk_wait_read0();
+                    mbar_arrive(q_empty + sb);
+                }
+                __syncwarp();
+            }
+            sched_release(sc, ks, true);
+        }
+        if (lane == 0) bulk_wait0();
     } else {
         // ------------------------------------------------------------ softmax / epilogue
         const int r = threadIdx.x;  // tile row = TMEM lane
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
         uint32_t g = 0;
+        int nq = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
@@ -461,13 +511,19 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     mbar_wait(freeb + gp % NBUF, (gp / NBUF) & 1);
                 }
                 tc_fence_after();
+                // O / Z -> bf16 staged in this item's Q buffer (its last S is done), one TMA store
+                const int qb = nq & 1;
+                ++nq;
+                uint8_t *sO = sQ + qb * 16384;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     float o[32];
                     tmem_ld32(tl + COL_O + hh * 32, o);
                     tmem_ld_wait();
-                    if (valid) store_row_bf16(orow, o, f, hh);
+                    stage_row_bf16(sO, r, o, f, hh);
                 }
+                fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
+                mbar_arrive(staged + qb);
                 tc_fence_before();
             } else if (valid) {
                 zero_row_bf16(orow);
@@ -479,7 +535,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
     __syncthreads();
     sched_finish(p);
-    if (warp == 5) {
+    if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<Cfg<B>::FWD_COLS>(tmem);
     }
@@ -490,11 +546,13 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 // block J: S, dP into one of NBUF TMEM buffer pairs -> dS = exp(S c - lse)(dP - D),
 // packed bf16 over S -> dQ += dS K_J (A from TMEM).  No atomics, no fp32 round trip.
 template <int B>
-__global__ void __launch_bounds__(TC_THREADS, Cfg<B>::DQ_CTAS)
+__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DQ_MW), Cfg<B>::DQ_CTAS)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmK,
-                      const __grid_constant__ CUtensorMap tmV, TcParams p) {
-    constexpr int NST = Cfg<B>::DQ_NST, NBUF = Cfg<B>::DQ_NBUF;
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdQ, TcParams p) {
+    constexpr int NST = Cfg<B>::DQ_NST, NBUF = Cfg<B>::DQ_NBUF, MW = Cfg<B>::DQ_MW;
+    constexpr int CW = B * 4 / MW;  // columns of a block per softmax warp (B or B/2)
+    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2;
     constexpr uint32_t BUFW = 2 * B;  // S at b*BUFW, dP at b*BUFW + B
     constexpr uint32_t COL_DQ = NBUF * BUFW;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;
@@ -512,29 +570,33 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
              *kv_empty = kv_full + NST;
     Sched sc = make_sched(sSched, kv_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
+    uint64_t *staged = kv_empty + NST + 9;  // [2]: dQ of the item using Q buffer qb staged
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(ds_full + i, 128); mbar_init(freeb + i, 1); }
+        // q_empty: the last MMA of the item, and the epilogue's TMA store of dQ (staged in the
+        // same buffer) having read shared memory
+        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 2); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(ds_full + i, 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(o_full, 1);
-        mbar_init(o_empty, 128);
+        mbar_init(o_empty, 32 * MW);
         mbar_init(dq_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
-        sched_init(sc);
+        for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
+        sched_init(sc, 2 + MW);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<Cfg<B>::DQ_COLS>(tmem_slot);
+    if (warp == W_MMA) tmem_alloc<Cfg<B>::DQ_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int nitems = (int)(p.bh * p.ntiles);
 
-    if (warp == 4) {
+    if (warp == W_PROD) {
         if (lane == 0) {
             prefetch_tmap(&tmQ); prefetch_tmap(&tmdO); prefetch_tmap(&tmO);
-            prefetch_tmap(&tmK); prefetch_tmap(&tmV);
+            prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmdQ);
         }
         int st = 0, nq = 0;
         uint32_t ph = 0;
@@ -573,7 +635,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             }
             __syncwarp();
         }
-    } else if (warp == 5) {
+    } else if (warp == W_MMA) {
         // MMA issuer: converged warp, one elected lane issues; S/dP up to NBUF blocks ahead
         int sst = 0, pst = 0, nq = 0;
         uint32_t sph = 0, g = 0;
@@ -617,7 +679,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DQ, tmem + b * BUFW + 8 * k, dK0 + 128 * k, IDESC_DQ, (pj > 0) || (k > 0));
+                                mma_bf16_ts(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
+                                            (pj > 0) || (k > 0));
                             mma_commit(freeb + b);
                             mma_commit(kv_empty + pst);
                             if (pj == cnt - 1) { mma_commit(dq_full); mma_commit(q_empty + qb); }
@@ -630,10 +693,34 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             }
             sched_release(sc, ks, true);
         }
+    } else if (warp == W_STORE) {
+        // storer: once the softmax warps have staged an item's output tile(s) in shared
+        // memory, one TMA store per tile; the buffer is released when the store has read it
+        int ns = 0;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int bh = h[1], t = h[2], cnt = h[3];
+            if (cnt > 0) {
+                const int sb = ns & 1;
+                mbar_wait(staged + sb, (ns >> 1) & 1);
+                ++ns;
+                if (lane == 0) {
+                    tma_store_3d(&tmdQ, sQ + sb * 16384, 0, t * 128, bh);
+                    bulk_commit();
+                    bulk_wait_read0();
+                    mbar_arrive(q_empty + sb);
+                }
+                __syncwarp();
+            }
+            sched_release(sc, ks, true);
+        }
+        if (lane == 0) bulk_wait0();
     } else {
-        const int r = threadIdx.x;  // query row of the tile
+        const int r = (warp & 3) * 32 + lane;  // query row of the tile = TMEM lane
+        const int wg = warp >> 2;              // column group: columns [wg*CW, wg*CW + CW) of each block
         const int slot = r / B;
-        const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+        const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         uint32_t dq_ph = 0, g = 0;
         int nq = 0;
         const float sl2 = p.scale_log2;
@@ -647,7 +734,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             __nv_bfloat16 *dqrow =
                 static_cast<__nv_bfloat16 *>(p.dQ) + (int64_t)bh * p.stride_bh + (int64_t)row * p.stride_l;
             if (cnt == 0) {
-                if (valid) zero_row_bf16(dqrow);
+                if (valid && wg == 0) zero_row_bf16(dqrow);
                 sched_release(sc, ks, true);
                 continue;
             }
@@ -674,7 +761,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 }
             }
             mbar_arrive(o_empty);
-            if (valid) {
+            if (valid && wg == 0) {
                 p.D[(int64_t)bh * p.L + row] = Dr;
                 p.nlse2[(int64_t)bh * p.L + row] = nl2;
             }
@@ -685,12 +772,13 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
-                for (int hh = 0; hh < B / 32; ++hh) {
+                for (int hh = 0; hh < CW / 32; ++hh) {
+                    const uint32_t c32 = wg * CW + hh * 32;  // this warp's 32-column chunk
                     uint32_t pk[16];
                     if (active) {
                         float sv[32], dp[32];
-                        tmem_ld32(tl + cs + hh * 32, sv);
-                        tmem_ld32(tl + cs + B + hh * 32, dp);
+                        tmem_ld32(tl + cs + c32, sv);
+                        tmem_ld32(tl + cs + B + c32, dp);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
@@ -702,7 +790,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 #pragma unroll
                         for (int i = 0; i < 16; ++i) pk[i] = 0u;
                     }
-                    tmem_st16(tl + cs + hh * 16, pk);  // packed dS over the consumed S columns
+                    tmem_st16(tl + cs + c32, pk);  // packed dS over this warp's own consumed S columns
                 }
                 tmem_st_wait();
                 tc_fence_before();
@@ -711,13 +799,18 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             mbar_wait(dq_full, dq_ph);
             dq_ph ^= 1;
             tc_fence_after();
+            // dQ -> bf16 staged in this item's Q buffer (every MMA of the item is done), one TMA store
+            uint8_t *sdQ = sQ + qb * 16384;
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
+                if (MW == 8 && hh != wg) continue;  // two warpgroups: one 32-column half each
                 float v[32];
                 tmem_ld32(tl + COL_DQ + hh * 32, v);
                 tmem_ld_wait();
-                if (valid) store_row_bf16(dqrow, v, p.scale, hh);
+                stage_row_bf16(sdQ, r, v, p.scale, hh);
             }
+            fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
+            mbar_arrive(staged + qb);
             tc_fence_before();
             g += cnt;
             sched_release(sc, ks, true);
@@ -725,7 +818,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     }
     __syncthreads();
     sched_finish(p);
-    if (warp == 5) {
+    if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<Cfg<B>::DQ_COLS>(tmem);
     }
@@ -737,11 +830,13 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 // blocks ahead of the softmax warps); P^T, dS^T packed over them feed dV += P^T dO_I,
 // dK += dS^T Q_I as A operands from tensor memory.
 template <int B>
-__global__ void __launch_bounds__(TC_THREADS, Cfg<B>::DKV_CTAS)
+__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DKV_MW), Cfg<B>::DKV_CTAS)
 attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                        TcParams p) {
-    constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF;
+                        const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcParams p) {
+    constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF, MW = Cfg<B>::DKV_MW;
+    constexpr int CW = B * 4 / MW;  // columns of a block per softmax warp (B or B/2)
+    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2;
     constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
     constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;
     constexpr uint32_t TILE = B * 128;
@@ -759,36 +854,46 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
              *p_full = s_full + NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
     Sched sc = make_sched(sSched, q_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
+    uint64_t *staged = q_empty + NST + 9;  // [2]: dK/dV of the item using K/V buffer kb staged
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
-        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); mbar_init(freeb + i, 1); }
+        // kv_empty: the last S^T/dP^T MMA of the item, and the epilogue's TMA store of dK/dV
+        // (staged in the same buffer) having read shared memory
+        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 2); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(acc_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        sched_init(sc);
+        for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
+        sched_init(sc, 2 + MW);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
+    if (warp == W_MMA) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int nitems = (int)(p.bh * p.ntiles);
 
-    if (warp == 4) {
-        if (lane == 0) { prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmQ); prefetch_tmap(&tmdO); }
+    if (warp == W_PROD) {
+        Tracer tr(p, 0);
+        if (lane == 0) {
+            prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmQ); prefetch_tmap(&tmdO);
+            prefetch_tmap(&tmdK); prefetch_tmap(&tmdV);
+        }
         int st = 0, nk = 0;
         uint32_t ph = 0;
         for (int ks = 0;; ++ks) {
             const int item = sched_produce(sc, ks, p, nitems, false);
             if (item < 0) break;
+            if (lane == 0) tr.ev(1);
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *rows = sc.col + (ks & 3) * SCHED_CAP;
             if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the copies
                 const int kb = nk & 1;
                 if (nk >= 2) mbar_wait(kv_empty + kb, ((nk >> 1) - 1) & 1);
+                if (lane == 0) tr.ev(2);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(kv_full + kb, 32768);
                     tma_load_3d(sKV + kb * 32768, &tmK, kv_full + kb, 0, t * 128, bh);
@@ -799,6 +904,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 for (int j = 0; j < cnt; ++j) {
                     const int I = rows[j];
                     mbar_wait(q_empty + st, ph ^ 1);
+                    if (lane == 0) tr.ev(3);
                     uint8_t *stg = sStage + st * STAGE;
                     if (elect_one()) {
                         mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
@@ -813,17 +919,20 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             }
             __syncwarp();
         }
-    } else if (warp == 5) {
+    } else if (warp == W_MMA) {
         // MMA issuer: converged warp, one elected lane issues; S^T/dP^T up to NBUF blocks ahead
+        Tracer tr(p, 1);
         int sst = 0, pst = 0, nk = 0;
         uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
+            if (lane == 0) tr.ev(10);
             const int cnt = h[3];
             if (cnt > 0) {
                 const int kb = nk & 1;
                 mbar_wait(kv_full + kb, (nk >> 1) & 1);
+                if (lane == 0) tr.ev(11);
                 tc_fence_after();
                 ++nk;
                 const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
@@ -834,6 +943,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
                         mbar_wait(q_full + sst, sph);
                         if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                        if (lane == 0) tr.ev(12);
                         tc_fence_after();
                         uint8_t *stg = sStage + sst * STAGE;
                         const uint32_t cs = b * BUFW;
@@ -854,6 +964,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     {  // dV += P^T dO, dK += dS^T Q for block pj (A from TMEM)
                         const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
                         mbar_wait(p_full + b, u & 1);
+                        if (lane == 0) tr.ev(13);
                         tc_fence_after();
                         uint8_t *stg = sStage + pst * STAGE;
                         const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
@@ -862,10 +973,12 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DV, tmem + cs + 8 * k, ddO0 + 128 * k, IDESC_DKV, (pj > 0) || (k > 0));
+                                mma_bf16_ts(tmem + COL_DV, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
+                                            (pj > 0) || (k > 0));
 #pragma unroll
                             for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 8 * k, dQ0 + 128 * k, IDESC_DKV, (pj > 0) || (k > 0));
+                                mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
+                                            (pj > 0) || (k > 0));
                             mma_commit(freeb + b);
                             mma_commit(q_empty + pst);
                             if (pj == cnt - 1) mma_commit(acc_full);
@@ -878,16 +991,44 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             }
             sched_release(sc, ks, true);
         }
-    } else {
-        const int r = threadIdx.x;  // key row of the tile = TMEM lane
-        const int slot = r / B;
-        const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t a_ph = 0, ph = 0, g = 0;
-        int st = 0;
-        const float sl2 = p.scale_log2;
+    } else if (warp == W_STORE) {
+        // storer: once the softmax warps have staged an item's output tile(s) in shared
+        // memory, one TMA store per tile; the buffer is released when the store has read it
+        int ns = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
+            const int bh = h[1], t = h[2], cnt = h[3];
+            if (cnt > 0) {
+                const int sb = ns & 1;
+                mbar_wait(staged + sb, (ns >> 1) & 1);
+                ++ns;
+                if (lane == 0) {
+                    tma_store_3d(&tmdK, sKV + sb * 32768, 0, t * 128, bh);
+                    tma_store_3d(&tmdV, sKV + sb * 32768 + 16384, 0, t * 128, bh);
+                    bulk_commit();
+                    bulk_wait_read0();
+                    mbar_arrive(kv_empty + sb);
+                }
+                __syncwarp();
+            }
+            sched_release(sc, ks, true);
+        }
+        if (lane == 0) bulk_wait0();
+    } else {
+        const int r = (warp & 3) * 32 + lane;  // key row of the tile = TMEM lane
+        const int wg = warp >> 2;              // column group: columns [wg*CW, wg*CW + CW) of each block
+        const int slot = r / B;
+        const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        uint32_t a_ph = 0, ph = 0, g = 0;
+        int st = 0, nk = 0;
+        const float sl2 = p.scale_log2;
+        Tracer tr(p, 2 + (threadIdx.x == 128));
+        const bool trc = threadIdx.x == 0 || threadIdx.x == 128;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            if (trc) tr.ev(20);
             const int bh = h[1], t = h[2], cnt = h[3];
             const int *msks = sc.msk + (ks & 3) * SCHED_CAP;
             const int key = t * 128 + r;
@@ -897,7 +1038,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             __nv_bfloat16 *dvrow =
                 static_cast<__nv_bfloat16 *>(p.dV) + (int64_t)bh * p.stride_bh + (int64_t)key * p.stride_l;
             if (cnt == 0) {
-                if (valid) { zero_row_bf16(dkrow); zero_row_bf16(dvrow); }
+                if (valid && (MW == 4 || wg == 0)) zero_row_bf16(dkrow);
+                if (valid && (MW == 4 || wg == 1)) zero_row_bf16(dvrow);
                 sched_release(sc, ks, true);
                 continue;
             }
@@ -908,19 +1050,21 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 const float *sD = snl2 + 128;
                 const uint32_t gs = g + jj, sb = gs % NBUF;
                 mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dV/dK MMAs that read sb before
+                if (trc) tr.ev(21);
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
-                for (int hh = 0; hh < B / 32; ++hh) {
+                for (int hh = 0; hh < CW / 32; ++hh) {
+                    const uint32_t c32 = wg * CW + hh * 32;  // this warp's 32-column chunk
                     uint32_t pk[16], dk[16];
                     if (active) {
                         float sv[32], dp[32], nl[32], dd[32];
-                        tmem_ld32(tl + cs + hh * 32, sv);
-                        tmem_ld32(tl + cs + B + hh * 32, dp);
+                        tmem_ld32(tl + cs + c32, sv);
+                        tmem_ld32(tl + cs + B + c32, dp);
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {  // broadcast LDS.128 of the query block's offsets
-                            const float4 a = reinterpret_cast<const float4 *>(snl2 + hh * 32)[i];
-                            const float4 b = reinterpret_cast<const float4 *>(sD + hh * 32)[i];
+                            const float4 a = reinterpret_cast<const float4 *>(snl2 + c32)[i];
+                            const float4 b = reinterpret_cast<const float4 *>(sD + c32)[i];
                             nl[4 * i] = a.x; nl[4 * i + 1] = a.y; nl[4 * i + 2] = a.z; nl[4 * i + 3] = a.w;
                             dd[4 * i] = b.x; dd[4 * i + 1] = b.y; dd[4 * i + 2] = b.z; dd[4 * i + 3] = b.w;
                         }
@@ -936,37 +1080,58 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
 #pragma unroll
                         for (int i = 0; i < 16; ++i) { pk[i] = 0u; dk[i] = 0u; }
                     }
-                    // packed bf16 P^T / dS^T over the (already read) S^T / dP^T columns
-                    tmem_st16(tl + cs + hh * 16, pk);
-                    tmem_st16(tl + cs + B + hh * 16, dk);
+                    // packed bf16 P^T / dS^T over this warp's own (already read) S^T / dP^T columns
+                    tmem_st16(tl + cs + c32, pk);
+                    tmem_st16(tl + cs + B + c32, dk);
                 }
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(p_full + sb);
+                if (trc) tr.ev(22);
                 if (++st == NST) { st = 0; ph ^= 1; }
             }
             mbar_wait(acc_full, a_ph);
+            if (trc) tr.ev(23);
             a_ph ^= 1;
             tc_fence_after();
+            // dK, dV -> bf16 staged in this item's K/V buffer (free: every S^T/dP^T MMA is done),
+            // then one TMA store per tile (coalesced; rows past L clipped)
+            const int kb = nk & 1;
+            ++nk;
+            uint8_t *sdK = sKV + kb * 32768, *sdV = sdK + 16384;
+            if (MW == 8) {  // warpgroup 0 stages dK, warpgroup 1 stages dV
+                const uint32_t col = wg == 0 ? COL_DK : COL_DV;
+                uint8_t *dst = wg == 0 ? sdK : sdV;
+                const float f = wg == 0 ? p.scale : 1.f;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                float kv[32], vv[32];
-                tmem_ld32(tl + COL_DK + hh * 32, kv);
-                tmem_ld32(tl + COL_DV + hh * 32, vv);
-                tmem_ld_wait();
-                if (valid) {
-                    store_row_bf16(dkrow, kv, p.scale, hh);
-                    store_row_bf16(dvrow, vv, 1.f, hh);
+                for (int hh = 0; hh < 2; ++hh) {
+                    float v[32];
+                    tmem_ld32(tl + col + hh * 32, v);
+                    tmem_ld_wait();
+                    stage_row_bf16(dst, r, v, f, hh);
+                }
+            } else {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    float kv[32], vv[32];
+                    tmem_ld32(tl + COL_DK + hh * 32, kv);
+                    tmem_ld32(tl + COL_DV + hh * 32, vv);
+                    tmem_ld_wait();
+                    stage_row_bf16(sdK, r, kv, p.scale, hh);
+                    stage_row_bf16(sdV, r, vv, 1.f, hh);
                 }
             }
+            fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
+            mbar_arrive(staged + kb);
             tc_fence_before();
+            if (trc) tr.ev(24);
             g += cnt;
             sched_release(sc, ks, true);
         }
     }
     __syncthreads();
     sched_finish(p);
-    if (warp == 5) {
+    if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<Cfg<B>::DKV_COLS>(tmem);
     }
@@ -1078,15 +1243,16 @@ static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         SPION_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem<B>()));
         attr = true;
     }
-    CUtensorMap mq, mk, mv;
+    CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mk, a.K, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
-        !make_map(&mv, a.V, a.L, a.bh, a.stride_bh, a.stride_l, B))
+        !make_map(&mv, a.V, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
+        !make_map(&mo, a.Oout, a.L, a.bh, a.stride_bh, a.stride_l, 128))
         return SPION_ERR_CUDA;
     TcParams p = base_params(a, 0, Cfg<B>::FWD_CTAS);
     p.O = a.Oout;
     p.lse_out = a.lse_out;
-    attn_fwd_tc_kernel<B><<<grid_for(p, Cfg<B>::FWD_CTAS), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, p);
+    attn_fwd_tc_kernel<B><<<grid_for(p, Cfg<B>::FWD_CTAS), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, mo, p);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
@@ -1099,7 +1265,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dkv_smem<B>()));
         attr = true;
     }
-    CUtensorMap mq128, mdo128, mo128, mkB, mvB, mk128, mv128, mqB, mdoB;
+    CUtensorMap mq128, mdo128, mo128, mkB, mvB, mk128, mv128, mqB, mdoB, mdq128, mdk128, mdv128;
     if (!make_map(&mq128, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mdo128, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mo128, a.O, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
@@ -1108,7 +1274,10 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         !make_map(&mk128, a.K, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mv128, a.V, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mqB, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
-        !make_map(&mdoB, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, B))
+        !make_map(&mdoB, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
+        !make_map(&mdq128, a.dQ, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
+        !make_map(&mdk128, a.dK, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
+        !make_map(&mdv128, a.dV, a.L, a.bh, a.stride_bh, a.stride_l, 128))
         return SPION_ERR_CUDA;
     // 1) dQ (row tiles) and D = rowsum(dO * O)
     TcParams p = base_params(a, 1, Cfg<B>::DQ_CTAS);
@@ -1117,7 +1286,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     p.D = const_cast<float *>(a.D);
     p.nlse2 = a.nlse2;
     p.dQ = a.dQ;
-    attn_bwd_dq_tc_kernel<B><<<grid_for(p, Cfg<B>::DQ_CTAS), TC_THREADS, dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, p);
+    attn_bwd_dq_tc_kernel<B><<<grid_for(p, Cfg<B>::DQ_CTAS), bwd_threads(Cfg<B>::DQ_MW), dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, mdq128, p);
     SPION_LAUNCH_CHECK();
     // 2) dK, dV (column tiles)
     TcParams q = base_params(a, 2, Cfg<B>::DKV_CTAS);
@@ -1125,7 +1294,8 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     q.D = const_cast<float *>(a.D);
     q.dK = a.dK;
     q.dV = a.dV;
-    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), TC_THREADS, dkv_smem<B>(), s>>>(mk128, mv128, mqB, mdoB, q);
+    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), bwd_threads(Cfg<B>::DKV_MW), dkv_smem<B>(), s>>>(
+        mk128, mv128, mqB, mdoB, mdk128, mdv128, q);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
