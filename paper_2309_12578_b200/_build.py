@@ -25,17 +25,20 @@ def _needs(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out_dir: str = OUT_DIR, defines=()) -> str:
+    """Compile csrc/*.cu into out_dir/libspion.so; `defines` (e.g. ["-DSPION_PING=0"]) build a
+    variant for A/B measurements (tools/build_variant.py)."""
+    SO = os.path.join(out_dir, "libspion.so")
+    os.makedirs(os.path.join(out_dir, "obj"), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "spion.h")]
     objs = []
     jobs = []
     for s in srcs:
-        o = os.path.join(OUT_DIR, "obj", os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(out_dir, "obj", os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _needs(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v", "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *defines, "-Xptxas", "-v", "-c", s, "-o", o]
             jobs.append(cmd)
 
     def run(cmd):

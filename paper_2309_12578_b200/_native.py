@@ -5,7 +5,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(PKG, "lib", "libspion.so")
+# SPION_LIB: an alternative build of the same library (A/B experiments, tools/build_variant.py)
+SO_PATH = os.environ.get("SPION_LIB") or os.path.join(PKG, "lib", "libspion.so")
 
 OK = 0
 STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace", 6: "cuda", 7: "unsupported"}

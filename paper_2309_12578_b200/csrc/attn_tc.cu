@@ -22,12 +22,12 @@
 //           -> dV += P^T dO_I, dK += dS^T Q_I (TMEM);  dK * scale -> bf16.
 //
 // Warp roles: warps 0..MW-1 softmax / epilogue (thread = TMEM lane = tile row;
-// with MW = 8 the two warpgroups take the two column halves of every block),
+// with MW = 8 the two warpgroups take alternate blocks, so the TMEM loads and
+// exponentials of one overlap the other's),
 // warp MW scheduler + TMA producer, warp MW+1 MMA issuer (one elected lane of a
 // converged warp) and TMEM allocator.  The forward has MW = 4; the backward
-// kernels MW = 8 where one CTA owns the SM.  A softmax warp writes its packed bf16
-// P / dS over the first half of each 32-column chunk it has read itself, so the
-// two warpgroups never race on TMEM columns.  One CTA per SM owns all 512 TMEM
+// kernels MW = 8 where one CTA owns the SM.  A softmax thread writes its packed bf16
+// P / dS over the first half of each 32-column chunk it has read itself.  One CTA per SM owns all 512 TMEM
 // columns: S (and dP) rotate through NBUF buffers so the MMA warp runs up to NBUF
 // blocks ahead of the softmax warps; P / dS are written back
 // into TMEM as packed bf16 and consumed as the A operand of the next MMA
@@ -43,13 +43,18 @@
 #include "attn.cuh"
 #include "tc_ptx.cuh"
 
+// compile-time knobs (A/B builds: tools/build_variant.py)
+#ifndef SPION_PING
+#define SPION_PING 1
+#endif
+
 namespace spion {
 
 using namespace tc;
 
-static constexpr int TC_THREADS = 224;  // forward: 4 softmax warps + producer + MMA + storer
-// backward: MW softmax warps, then the producer, MMA and storer warps
-__host__ __device__ constexpr int bwd_threads(int mw) { return 32 * (mw + 3); }
+static constexpr int TC_THREADS = 256;  // forward: 4 softmax warps + producer + S-MMA + storer + PV-MMA
+// backward: MW softmax warps, then the producer, S-MMA, storer and second MMA warps
+__host__ __device__ constexpr int bwd_threads(int mw) { return 32 * (mw + 4); }
 // Per-kernel, per-B configuration.  CTAS CTAs per SM share the 512 TMEM columns
 // (COLS each) and ~227 KB of shared memory; NBUF score buffers let the MMA warp run
 // up to NBUF blocks ahead of the softmax warps; TMA rings have NST >= NBUF stages
@@ -68,6 +73,8 @@ template <int B> struct Cfg {
     // softmax warps of the backward kernels: two warpgroups (each takes half of a block's
     // columns) where one CTA owns the SM, one warpgroup where two CTAs share it
     static constexpr int DQ_MW = DQ_CTAS == 1 ? 8 : 4, DKV_MW = DKV_CTAS == 1 ? 8 : 4;
+    // with two softmax warpgroups: alternate blocks (ping-pong) or split every block's columns
+    static constexpr bool PING = SPION_PING;
     static_assert(FWD_NST >= FWD_NBUF && DQ_NST >= DQ_NBUF && DKV_NST >= DKV_NBUF, "ring shallower than look-ahead");
 };
 static constexpr int SCHED_CAP = 128;  // max entries of one tile list (nblk <= 128)
@@ -108,7 +115,7 @@ struct Tracer {
         if (base && n < 1024) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            base[2 * n] = (unsigned long long)id;
+            base[2 * n] = (unsigned long long)id | ((unsigned long long)clock64() << 8);
             base[2 * n + 1] = t;
             ++n;
         }
@@ -257,7 +264,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, 64, false, true);
     constexpr uint32_t COL_O = NBUF * B;  // S / P buffer b at columns [B b, B b + B)
-    constexpr int W_PROD = 4, W_MMA = 5, W_STORE = 6;
+    constexpr int W_PROD = 4, W_MMA = 5, W_STORE = 6, W_MMA2 = 7;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
@@ -282,7 +289,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); mbar_init(freeb + i, 1); }
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         for (int i = 0; i < 2; ++i) mbar_init(staged + i, 128);
-        sched_init(sc, 6);
+        sched_init(sc, 7);
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::FWD_COLS>(tmem_slot);
@@ -326,11 +333,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             __syncwarp();
         }
     } else if (warp == W_MMA) {
-        // ------------------------------------------------------------ MMA issuer (converged warp,
-        // one elected lane issues): S for up to NBUF blocks ahead, then P.V as P arrives
-        int sst = 0, pst = 0, nq = 0;  // ring cursors of the next S and the next P.V
-        uint32_t sph = 0;
-        uint32_t g = 0;                // global block counter (buffer = g % NBUF)
+        // ------------------------------------------------------------ S issuer (converged warp,
+        // one elected lane issues): S = Q K_J^T up to NBUF blocks ahead of the softmax
+        int sst = 0, nq = 0;
+        uint32_t sph = 0, g = 0;  // global block counter (buffer = g % NBUF)
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -341,42 +347,51 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tc_fence_after();
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
-                int sj = 0;  // next S of this item
-                for (int pj = 0; pj < cnt; ++pj) {
-                    for (; sj < cnt && sj < pj + NBUF; ++sj) {  // S(sj) = Q K_J^T into buffer (g+sj) % NBUF
-                        const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
-                        mbar_wait(kv_full + sst, sph);
-                        if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
-                        tc_fence_after();
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
-                        if (elect_one()) {
+                for (int sj = 0; sj < cnt; ++sj) {
+                    const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
+                    mbar_wait(kv_full + sst, sph);
+                    if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                    tc_fence_after();
+                    const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
+                    if (elect_one()) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                mma_bf16_ss(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
-                            mma_commit(s_full + b);
-                            if (sj == cnt - 1) mma_commit(q_empty + qb);
-                        }
-                        __syncwarp();
-                        if (++sst == NST) { sst = 0; sph ^= 1; }
+                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                        mma_commit(s_full + b);
+                        if (sj == cnt - 1) mma_commit(q_empty + qb);
                     }
-                    {  // O += P(pj) V(pj), P from TMEM
-                        const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
-                        mbar_wait(p_full + b, u & 1);
-                        tc_fence_after();
-                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + pst * STG + KV_BYTES));
-                        if (elect_one()) {
-#pragma unroll
-                            for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
-                            mma_commit(freeb + b);
-                            mma_commit(kv_empty + pst);
-                        }
-                        __syncwarp();
-                        if (++pst == NST) pst = 0;
-                    }
+                    __syncwarp();
+                    if (++sst == NST) { sst = 0; sph ^= 1; }
                 }
                 g += cnt;
             }
+            sched_release(sc, ks, true);
+        }
+    } else if (warp == W_MMA2) {
+        // ------------------------------------------------------------ P.V issuer: O += P_J V_J
+        // (P from TMEM) as each P arrives.  A second issuing warp, so the tensor pipe is fed by
+        // whichever stream is ready while the other waits (a commit stalls its issuing thread).
+        int pst = 0;
+        uint32_t g = 0;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int cnt = h[3];
+            for (int pj = 0; pj < cnt; ++pj) {
+                const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                mbar_wait(p_full + b, u & 1);
+                tc_fence_after();
+                const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + pst * STG + KV_BYTES));
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < B / 16; ++k)
+                        mma_bf16_ts(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
+                    mma_commit(freeb + b);
+                    mma_commit(kv_empty + pst);  // S(pj) (K) completed before P(pj) existed
+                }
+                __syncwarp();
+                if (++pst == NST) pst = 0;
+            }
+            g += cnt;
             sched_release(sc, ks, true);
         }
     } else if (warp == W_STORE) {
@@ -551,8 +566,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdQ, TcParams p) {
     constexpr int NST = Cfg<B>::DQ_NST, NBUF = Cfg<B>::DQ_NBUF, MW = Cfg<B>::DQ_MW;
-    constexpr int CW = B * 4 / MW;  // columns of a block per softmax warp (B or B/2)
-    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2;
+    constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
+    constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
+    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3;
     constexpr uint32_t BUFW = 2 * B;  // S at b*BUFW, dP at b*BUFW + B
     constexpr uint32_t COL_DQ = NBUF * BUFW;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;
@@ -571,19 +587,21 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     Sched sc = make_sched(sSched, kv_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
     uint64_t *staged = kv_empty + NST + 9;  // [2]: dQ of the item using Q buffer qb staged
+    uint64_t *acc_empty = staged + 2;       // the epilogue has read the dQ accumulator
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         // q_empty: the last MMA of the item, and the epilogue's TMA store of dQ (staged in the
         // same buffer) having read shared memory
         for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 2); }
-        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(ds_full + i, 32 * MW); mbar_init(freeb + i, 1); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(ds_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(o_full, 1);
         mbar_init(o_empty, 32 * MW);
         mbar_init(dq_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
-        sched_init(sc, 2 + MW);
+        mbar_init(acc_empty, 32 * MW);
+        sched_init(sc, 3 + MW);
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DQ_COLS>(tmem_slot);
@@ -636,8 +654,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             __syncwarp();
         }
     } else if (warp == W_MMA) {
-        // MMA issuer: converged warp, one elected lane issues; S/dP up to NBUF blocks ahead
-        int sst = 0, pst = 0, nq = 0;
+        // S / dP issuer (converged warp, one elected lane issues), up to NBUF blocks ahead
+        int sst = 0, nq = 0;
         uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
@@ -650,44 +668,57 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
                 const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
-                int sj = 0;
+                for (int sj = 0; sj < cnt; ++sj) {
+                    const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
+                    mbar_wait(kv_full + sst, sph);
+                    if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t cs = b * BUFW;
+                    const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
+                    const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + sst * STG + KV_BYTES));
+                    if (elect_one()) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
+                        mma_commit(s_full + b);
+                        if (sj == cnt - 1) mma_commit(q_empty + qb);  // Q, dO no longer read
+                    }
+                    __syncwarp();
+                    if (++sst == NST) { sst = 0; sph ^= 1; }
+                }
+                g += cnt;
+            }
+            sched_release(sc, ks, true);
+        }
+    } else if (warp == W_MMA2) {
+        // dQ issuer: dQ += dS_J K_J (dS from TMEM) as each dS arrives; a second issuing warp so
+        // the tensor pipe is fed while the other waits (a commit stalls its issuing thread)
+        int pst = 0, na = 0;
+        uint32_t g = 0;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int cnt = h[3];
+            if (cnt > 0) {
+                if (na > 0) mbar_wait(acc_empty, (na - 1) & 1);  // the last item's dQ was read
+                ++na;
                 for (int pj = 0; pj < cnt; ++pj) {
-                    for (; sj < cnt && sj < pj + NBUF; ++sj) {  // S(sj), dP(sj)
-                        const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
-                        mbar_wait(kv_full + sst, sph);
-                        if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
-                        tc_fence_after();
-                        const uint32_t cs = b * BUFW;
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
-                        const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + sst * STG + KV_BYTES));
-                        if (elect_one()) {
+                    const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                    mbar_wait(ds_full + b, u & 1);
+                    tc_fence_after();
+                    const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + pst * STG));
+                    if (elect_one()) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                mma_bf16_ss(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
-                            mma_commit(s_full + b);
-                        }
-                        __syncwarp();
-                        if (++sst == NST) { sst = 0; sph ^= 1; }
+                        for (int k = 0; k < B / 16; ++k)
+                            mma_bf16_ts(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
+                                        (pj > 0) || (k > 0));
+                        mma_commit(freeb + b);
+                        mma_commit(kv_empty + pst);
+                        if (pj == cnt - 1) mma_commit(dq_full);
                     }
-                    {  // dQ += dS(pj) K(pj), dS from TMEM
-                        const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
-                        mbar_wait(ds_full + b, u & 1);
-                        tc_fence_after();
-                        const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + pst * STG));
-                        if (elect_one()) {
-#pragma unroll
-                            for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
-                                            (pj > 0) || (k > 0));
-                            mma_commit(freeb + b);
-                            mma_commit(kv_empty + pst);
-                            if (pj == cnt - 1) { mma_commit(dq_full); mma_commit(q_empty + qb); }
-                        }
-                        __syncwarp();
-                        if (++pst == NST) pst = 0;
-                    }
+                    __syncwarp();
+                    if (++pst == NST) pst = 0;
                 }
                 g += cnt;
             }
@@ -718,7 +749,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         if (lane == 0) bulk_wait0();
     } else {
         const int r = (warp & 3) * 32 + lane;  // query row of the tile = TMEM lane
-        const int wg = warp >> 2;              // column group: columns [wg*CW, wg*CW + CW) of each block
+        const int wg = warp >> 2;              // warpgroup: alternate blocks (MW = 8); epilogue halves
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         uint32_t dq_ph = 0, g = 0;
@@ -765,15 +796,17 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 p.D[(int64_t)bh * p.L + row] = Dr;
                 p.nlse2[(int64_t)bh * p.L + row] = nl2;
             }
-            for (int jj = 0; jj < cnt; ++jj) {
+            // two warpgroups (MW = 8) take alternate blocks, so one's TMEM loads and exponentials
+            // overlap the other's; a thread handles every column of its row of the block
+            for (int jj = (PP ? wg : 0); jj < cnt; jj += (PP ? 2 : 1)) {
                 const bool active = (msks[jj] >> slot) & 1;
                 const uint32_t gs = g + jj, sb = gs % NBUF;
                 mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dQ MMA that read sb before
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
-                for (int hh = 0; hh < CW / 32; ++hh) {
-                    const uint32_t c32 = wg * CW + hh * 32;  // this warp's 32-column chunk
+                for (int hh = 0; hh < CPT / 32; ++hh) {
+                    const uint32_t c32 = (PP ? 0 : wg * CPT) + hh * 32;  // 32-column chunk
                     uint32_t pk[16];
                     if (active) {
                         float sv[32], dp[32];
@@ -809,6 +842,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 tmem_ld_wait();
                 stage_row_bf16(sdQ, r, v, p.scale, hh);
             }
+            tc_fence_before();
+            mbar_arrive(acc_empty);  // the next item's first dQ MMA may overwrite the accumulator
             fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
             mbar_arrive(staged + qb);
             tc_fence_before();
@@ -835,8 +870,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcParams p) {
     constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF, MW = Cfg<B>::DKV_MW;
-    constexpr int CW = B * 4 / MW;  // columns of a block per softmax warp (B or B/2)
-    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2;
+    constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
+    constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
+    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3;
     constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
     constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;
     constexpr uint32_t TILE = B * 128;
@@ -855,17 +891,19 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     Sched sc = make_sched(sSched, q_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
     uint64_t *staged = q_empty + NST + 9;  // [2]: dK/dV of the item using K/V buffer kb staged
+    uint64_t *acc_empty = staged + 2;      // the epilogue has read the dK/dV accumulators
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         // kv_empty: the last S^T/dP^T MMA of the item, and the epilogue's TMA store of dK/dV
         // (staged in the same buffer) having read shared memory
         for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 2); }
-        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 32 * MW); mbar_init(freeb + i, 1); }
+        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(acc_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
         for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
-        sched_init(sc, 2 + MW);
+        mbar_init(acc_empty, 32 * MW);
+        sched_init(sc, 3 + MW);
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
@@ -920,9 +958,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             __syncwarp();
         }
     } else if (warp == W_MMA) {
-        // MMA issuer: converged warp, one elected lane issues; S^T/dP^T up to NBUF blocks ahead
+        // S^T / dP^T issuer (converged warp, one elected lane issues), up to NBUF blocks ahead
         Tracer tr(p, 1);
-        int sst = 0, pst = 0, nk = 0;
+        int sst = 0, nk = 0;
         uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
@@ -937,55 +975,70 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 ++nk;
                 const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
-                int sj = 0;
+                for (int sj = 0; sj < cnt; ++sj) {
+                    const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
+                    mbar_wait(q_full + sst, sph);
+                    if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                    if (lane == 0) tr.ev(12);
+                    tc_fence_after();
+                    uint8_t *stg = sStage + sst * STAGE;
+                    const uint32_t cs = b * BUFW;
+                    const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
+                    const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                    if (elect_one()) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
+                        mma_commit(s_full + b);
+                        if (sj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
+                    }
+                    __syncwarp();
+                    if (lane == 0) tr.ev(14);
+                    if (++sst == NST) { sst = 0; sph ^= 1; }
+                }
+                g += cnt;
+            }
+            sched_release(sc, ks, true);
+        }
+    } else if (warp == W_MMA2) {
+        // dV / dK issuer: dV += P^T dO_I, dK += dS^T Q_I (A from TMEM) as each block's P^T / dS^T
+        // arrives; a second issuing warp so the tensor pipe is fed while the other waits
+        Tracer tr(p, 4);
+        int pst = 0, na = 0;
+        uint32_t g = 0;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            const int cnt = h[3];
+            if (cnt > 0) {
+                if (na > 0) mbar_wait(acc_empty, (na - 1) & 1);  // the last item's dK/dV were read
+                ++na;
                 for (int pj = 0; pj < cnt; ++pj) {
-                    for (; sj < cnt && sj < pj + NBUF; ++sj) {  // S^T(sj), dP^T(sj)
-                        const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
-                        mbar_wait(q_full + sst, sph);
-                        if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
-                        if (lane == 0) tr.ev(12);
-                        tc_fence_after();
-                        uint8_t *stg = sStage + sst * STAGE;
-                        const uint32_t cs = b * BUFW;
-                        const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
-                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
-                        if (elect_one()) {
+                    const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                    mbar_wait(p_full + b, u & 1);
+                    if (lane == 0) tr.ev(13);
+                    tc_fence_after();
+                    uint8_t *stg = sStage + pst * STAGE;
+                    const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
+                    const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
+                    const uint32_t cs = b * BUFW;
+                    if (elect_one()) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
+                        for (int k = 0; k < B / 16; ++k)
+                            mma_bf16_ts(tmem + COL_DV, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
+                                        (pj > 0) || (k > 0));
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                mma_bf16_ss(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
-                            mma_commit(s_full + b);
-                            if (sj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
-                        }
-                        __syncwarp();
-                        if (++sst == NST) { sst = 0; sph ^= 1; }
+                        for (int k = 0; k < B / 16; ++k)
+                            mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
+                                        (pj > 0) || (k > 0));
+                        mma_commit(freeb + b);
+                        mma_commit(q_empty + pst);
+                        if (pj == cnt - 1) mma_commit(acc_full);
                     }
-                    {  // dV += P^T dO, dK += dS^T Q for block pj (A from TMEM)
-                        const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
-                        mbar_wait(p_full + b, u & 1);
-                        if (lane == 0) tr.ev(13);
-                        tc_fence_after();
-                        uint8_t *stg = sStage + pst * STAGE;
-                        const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
-                        const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
-                        const uint32_t cs = b * BUFW;
-                        if (elect_one()) {
-#pragma unroll
-                            for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DV, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
-                                            (pj > 0) || (k > 0));
-#pragma unroll
-                            for (int k = 0; k < B / 16; ++k)
-                                mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
-                                            (pj > 0) || (k > 0));
-                            mma_commit(freeb + b);
-                            mma_commit(q_empty + pst);
-                            if (pj == cnt - 1) mma_commit(acc_full);
-                        }
-                        __syncwarp();
-                        if (++pst == NST) pst = 0;
-                    }
+                    __syncwarp();
+                    if (lane == 0) tr.ev(15);
+                    if (++pst == NST) pst = 0;
                 }
                 g += cnt;
             }
@@ -1017,7 +1070,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         if (lane == 0) bulk_wait0();
     } else {
         const int r = (warp & 3) * 32 + lane;  // key row of the tile = TMEM lane
-        const int wg = warp >> 2;              // column group: columns [wg*CW, wg*CW + CW) of each block
+        const int wg = warp >> 2;              // warpgroup: alternate blocks (MW = 8); epilogue halves
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         uint32_t a_ph = 0, ph = 0, g = 0;
@@ -1043,7 +1096,13 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 sched_release(sc, ks, true);
                 continue;
             }
+            // two warpgroups (MW = 8) take alternate blocks, so one's TMEM loads and exponentials
+            // overlap the other's; a thread handles every column of its row of the block
             for (int jj = 0; jj < cnt; ++jj) {
+                if (PP && (jj & 1) != wg) {
+                    if (++st == NST) { st = 0; ph ^= 1; }
+                    continue;
+                }
                 const bool active = (msks[jj] >> slot) & 1;
                 mbar_wait(q_full + st, ph);  // lse_I, D_I
                 const float *snl2 = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
@@ -1054,8 +1113,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
-                for (int hh = 0; hh < CW / 32; ++hh) {
-                    const uint32_t c32 = wg * CW + hh * 32;  // this warp's 32-column chunk
+                for (int hh = 0; hh < CPT / 32; ++hh) {
+                    const uint32_t c32 = (PP ? 0 : wg * CPT) + hh * 32;  // 32-column chunk
                     uint32_t pk[16], dk[16];
                     if (active) {
                         float sv[32], dp[32], nl[32], dd[32];
@@ -1121,6 +1180,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     stage_row_bf16(sdV, r, vv, 1.f, hh);
                 }
             }
+            tc_fence_before();
+            mbar_arrive(acc_empty);    // the next item's first dV/dK MMAs may overwrite the accumulators
             fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
             mbar_arrive(staged + kb);
             tc_fence_before();

@@ -92,6 +92,13 @@ def syn_scores(L: int, B: int, heads: int = 4, seed: int = 11, n_stripes: int = 
     return acc.clamp_(0.0, 1.0)
 
 
+def lra_scores(L: int, B: int, seed: int = 1, device="cpu") -> torch.Tensor:
+    """The benchmark's score matrix: ``syn_scores`` with 4 heads and n/8 stripe columns
+    (n = L/B, at least 2), so the flood fill at alpha = 75 lands near the north star's
+    ~10 % block density at every LRA shape."""
+    return syn_scores(L, B, heads=4, seed=seed, n_stripes=max(2, (L // B) // 8), device=device)
+
+
 def block_density(mask: np.ndarray) -> float:
     return float(np.asarray(mask).astype(bool).mean())
 

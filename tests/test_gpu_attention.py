@@ -167,7 +167,7 @@ def test_full_size_sampled(cfg):
     spion = _spion()
     c = FULL[cfg]
     L, B, bh, d = c["L"], c["B"], c["bh"], 64
-    A = synth.syn_scores(L, B, heads=4, seed=1)
+    A = synth.lra_scores(L, B, seed=1)
     bp = spion.pattern(A.to(DEV), B, filter=31, alpha=c["alpha"], sync=True)
     fl, _, _ = oracle.pattern(A.numpy(), B, 31, c["alpha"])
     n = L // B

@@ -1,0 +1,74 @@
+// mufu_bench.cu — throughput of ex2 variants per SM: f32 (MUFU.EX2), f16x2 and bf16x2 packed forms,
+// and a Cody-Waite + degree-3 polynomial exp2 on the FMA pipe.  Timing only.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdio.h>
+#include <stdint.h>
+template <int MODE>
+__global__ void k(int reps, long long *out, float *sink) {
+    float a[8];
+    uint32_t u[8];
+    for (int i = 0; i < 8; ++i) { a[i] = -0.001f * (threadIdx.x + i); u[i] = 0x3c003c00u + i; }
+    __syncthreads();
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (MODE == 0) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i])); }
+            else if (MODE == 1) { asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u[i])); }
+            else if (MODE == 2) { asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i])); }
+            else if (MODE == 4) {  // packed f32x2 poly exp2 on pairs
+                uint64_t x2, t2, j2, f2, p2;
+                float xa = a[i], xb = -a[i] * 0.5f;
+                asm("mov.b64 %0, {%1, %2};" : "=l"(x2) : "f"(xa), "f"(xb));
+                const uint64_t M = 0x4B4000004B400000ull, NM = 0xCB400000CB400000ull;
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(x2), "l"(M));
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(j2) : "l"(t2), "l"(NM));
+                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f2) : "l"(x2), "l"(j2));
+                const uint64_t C3 = 0x3D6357C53D6357C5ull, C2 = 0x3E75FDF03E75FDF0ull, C1 = 0x3F3172183F317218ull, C0 = 0x3F8000003F800000ull;
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p2) : "l"(C3), "l"(f2), "l"(C2));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p2) : "l"(p2), "l"(f2), "l"(C1));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p2) : "l"(p2), "l"(f2), "l"(C0));
+                uint32_t plo, phi, tlo, thi;
+                asm("mov.b64 {%0, %1}, %2;" : "=r"(plo), "=r"(phi) : "l"(p2));
+                asm("mov.b64 {%0, %1}, %2;" : "=r"(tlo), "=r"(thi) : "l"(t2));
+                a[i] = __int_as_float(plo + (tlo << 23)) + __int_as_float(phi + (thi << 23)) - 2.0f;
+            } else {
+                float x = a[i];
+                float t = x + 12582912.0f;
+                float j = t - 12582912.0f;
+                float f = x - j;
+                float p = fmaf(fmaf(fmaf(0.0555041f, f, 0.2402265f), f, 0.6931472f), f, 1.0f);
+                a[i] = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23)) - 1.0f;
+            }
+        }
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    float s = 0;
+    for (int i = 0; i < 8; ++i) s += a[i] + __uint_as_float(u[i]);
+    if (s == 1234.5f) sink[threadIdx.x] = s;
+}
+template <int MODE>
+void run(const char *name, int per) {
+    long long *d, h;
+    float *s;
+    cudaMalloc(&d, 8);
+    cudaMalloc(&s, 4096 * 4);
+    const int reps = 1000, threads = 1024;
+    k<MODE><<<1, threads>>>(reps, d, s);
+    k<MODE><<<1, threads>>>(reps, d, s);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("%-28s %6.2f instr/clk/SM  %6.2f exp2/clk/SM\n", name, (double)threads * reps * 8 / h, (double)threads * reps * 8 * per / h);
+}
+int main() {
+    run<0>("ex2.approx.ftz.f32", 1);
+    run<1>("ex2.approx.f16x2", 2);
+    run<2>("ex2.approx.ftz.bf16x2", 2);
+    run<3>("poly3 exp2 (FMA pipe)", 1);
+    run<4>("poly3 exp2 f32x2 (pairs)", 2);
+    return 0;
+}

@@ -13,7 +13,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "text"
 L, B, bh = {"image": (1024, 32, 256), "text": (4096, 64, 128), "listops": (2048, 64, 256)}[cfg]
 d = 64
 dev = torch.device("cuda:0")
-A = synth.syn_scores(L, B, heads=2, seed=1, device=dev)
+A = synth.lra_scores(L, B, seed=1, device=dev)
 q, k, v, do = synth.qkvdo(bh, L, d, seed=3, dtype=torch.bfloat16, device=dev)
 bp = spion.pattern(A, B, filter=31, alpha=75.0, sync=True)
 o, lse = spion.attn_fwd(q, k, v, bp)
@@ -22,18 +22,34 @@ for _ in range(3):
 torch.cuda.synchronize()
 lib = N.lib()
 lib.spion_debug_trace.restype = ctypes.c_int64
-R = 4
+R = 5
 buf = (ctypes.c_ulonglong * (R * 2048))()
 n = lib.spion_debug_trace(buf, R * 2048)
 a = np.array(buf[:n], dtype=np.uint64).reshape(R, 1024, 2)
 evs = []
+names = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "M S issue", 13: "M dVdK issue", 14: "M S issued", 15: "M dVdK issued", 16: "m S0", 17: "m S4", 18: "m S8",
+         20: "S item", 21: "S s_full", 22: "S p arrive", 23: "S acc_full", 24: "S epi done"}
+clk = []
+mm = []
 for role in range(R):
     for e, t in a[role]:
         if t:
-            evs.append((int(t), int(e), role))
+            evs.append((int(t), int(e) & 255, role))
+            clk.append((int(t), int(e) >> 8))
+            if role == 1 and (int(e) & 255) in (16, 17, 18): mm.append((int(e) & 255, int(e) >> 8))
+clk.sort()
+mm.sort(key=lambda x: x[1])
+d1 = [b[1] - a[1] for a, b in zip(mm, mm[1:]) if a[0] == 16 and b[0] == 17]
+d2 = [b[1] - a[1] for a, b in zip(mm, mm[1:]) if a[0] == 17 and b[0] == 18]
+raw = sorted([(int(e) >> 8, int(e) & 255) for e, t in a[1] if t])
+import os
+if os.environ.get("RAW"):
+    for c, e in raw[200:260]: print("   clk", c - raw[0][0], names.get(e, e))
+if d1: print("issue cycles: first 4 SS MMAs median %d, next 4 median %d" % (sorted(d1)[len(d1) // 2], sorted(d2)[len(d2) // 2]))
+print("SM clock during the trace: %.0f MHz" % ((clk[-1][1] - clk[0][1]) / (clk[-1][0] - clk[0][0]) * 1e3))
 evs.sort()
 t0 = evs[0][0]
-names = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "M S issue", 13: "M dVdK issue",
+names0 = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "M S issue", 13: "M dVdK issue", 14: "M S issued", 16: "m S0", 17: "m S4", 18: "m S8", 15: "M dVdK issued",
          20: "S item", 21: "S s_full", 22: "S p arrive", 23: "S acc_full", 24: "S epi done"}
 lim = int(sys.argv[2]) if len(sys.argv) > 2 else 120
 for t, e, r in evs[:lim]:
