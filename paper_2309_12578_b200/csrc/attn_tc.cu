@@ -47,14 +47,43 @@
 #ifndef SPION_PING
 #define SPION_PING 1
 #endif
+// timing-only debug builds (wrong results): skip the MMAs, or the softmax loads and math
+#ifndef SPION_DBG_NOMMA
+#define SPION_DBG_NOMMA 0
+#endif
+#ifndef SPION_DBG_NOSOFTMAX
+#define SPION_DBG_NOSOFTMAX 0
+#endif
+#ifndef SPION_SEPOUT  // output staging buffers separate from the per-item input tiles
+#define SPION_SEPOUT 0
+#endif
+#ifndef SPION_NSW  // 1: one S-MMA warp per buffer where one CTA owns the SM (0: a single S-MMA warp)
+#define SPION_NSW 0
+#endif
+#ifndef SPION_DKV_NBUF  // override of the dK/dV kernel's S^T/dP^T buffer count (0 = as many as fit)
+#define SPION_DKV_NBUF 0
+#endif
+#ifndef SPION_DBG_NOLOAD  // per-block operand tiles not loaded
+#define SPION_DBG_NOLOAD 0
+#endif
+#if SPION_DBG_NOMMA
+#define MMA_SS(...) ((void)0)
+#define MMA_TS(...) ((void)0)
+#else
+#define MMA_SS(...) mma_bf16_ss(__VA_ARGS__)
+#define MMA_TS(...) mma_bf16_ts(__VA_ARGS__)
+#endif
+#ifndef SPION_POLY  // of every 16 exponentials, how many run as a polynomial on the FMA pipe
+#define SPION_POLY 0
+#endif
 
 namespace spion {
 
 using namespace tc;
 
 static constexpr int TC_THREADS = 256;  // forward: 4 softmax warps + producer + S-MMA + storer + PV-MMA
-// backward: MW softmax warps, then the producer, S-MMA, storer and second MMA warps
-__host__ __device__ constexpr int bwd_threads(int mw) { return 32 * (mw + 4); }
+// backward: MW softmax warps, then the producer, S-MMA, storer, second MMA and NSW - 1 more S-MMA warps
+__host__ __device__ constexpr int bwd_threads(int mw, int nsw) { return 32 * (mw + 3 + nsw); }  // W_MMA3.. = MW + 4..
 // Per-kernel, per-B configuration.  CTAS CTAs per SM share the 512 TMEM columns
 // (COLS each) and ~227 KB of shared memory; NBUF score buffers let the MMA warp run
 // up to NBUF blocks ahead of the softmax warps; TMA rings have NST >= NBUF stages
@@ -68,16 +97,40 @@ template <int B> struct Cfg {
     static constexpr int DQ_NBUF = (DQ_COLS - 64) / (2 * B);   // S+dP buffers + dQ
     static constexpr int DQ_NST = B == 32 ? 3 : 8;             // K_J + V_J per stage
     static constexpr int DKV_CTAS = B == 32 ? 2 : 1, DKV_COLS = 512 / DKV_CTAS;
-    static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
-    static constexpr int DKV_NST = B == 32 ? 4 : 9;              // Q_I + dO_I + lse_I + D_I per stage
+    static constexpr int DKV_NBUF = SPION_DKV_NBUF > 0 ? SPION_DKV_NBUF : (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
+    // dK/dV staged for the TMA store in their own buffer (not over the item's K/V tiles), so
+    // the next-but-one item's K/V load need not wait for this item's store (one CTA per SM only)
+    static constexpr bool DKV_SEP = DKV_CTAS == 1 && SPION_SEPOUT;
+    static constexpr int DKV_NST = B == 32 ? 4 : (DKV_SEP ? 7 : 9);  // Q_I + dO_I + lse_I + D_I per stage
     // softmax warps of the backward kernels: two warpgroups (each takes half of a block's
     // columns) where one CTA owns the SM, one warpgroup where two CTAs share it
     static constexpr int DQ_MW = DQ_CTAS == 1 ? 8 : 4, DKV_MW = DKV_CTAS == 1 ? 8 : 4;
     // with two softmax warpgroups: alternate blocks (ping-pong) or split every block's columns
     static constexpr bool PING = SPION_PING;
+    // S-MMA issuing warps: where one CTA owns the SM, one per TMEM score buffer (warp w issues
+    // the blocks whose buffer is w), so one warp's per-block issue overhead (waits, descriptors,
+    // commits, reconvergence) is not the limit, and every buffer's uses (and every ring stage's,
+    // NST % NBUF == 0) stay in order within one warp, as mbarrier parity waits require
+    static constexpr int DQ_NSW = DQ_CTAS == 1 && SPION_NSW ? DQ_NBUF : 1;
+    static constexpr int DKV_NSW = DKV_CTAS == 1 && SPION_NSW ? DKV_NBUF : 1;
     static_assert(FWD_NST >= FWD_NBUF && DQ_NST >= DQ_NBUF && DKV_NST >= DKV_NBUF, "ring shallower than look-ahead");
 };
-static constexpr int SCHED_CAP = 128;  // max entries of one tile list (nblk <= 128)
+static constexpr int SCHED_CAP = 128;
+
+// 2^x on the FMA pipe (the SFU does 16 ex2/clk/SM, as many as this does on the FP32 pipe):
+// Cody-Waite split x = j + f with j = rint(x) taken from the low mantissa bits of x + 1.5*2^23,
+// f in [-0.5, 0.5]; 2^f by a degree-3 relative-minimax polynomial (max rel. error 1.0e-4, far
+// below the 2^-9 rounding of P / dS to bf16); 2^j added into the exponent field.  x <= -127
+// gives +0 (like ex2.approx.ftz underflow).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -127.f);
+    const float t = x + 12582912.f;
+    const float f = x - (t - 12582912.f);
+    const float q = fmaf(fmaf(fmaf(0.05500883f, f, 0.24221103f), f, 0.69328296f), f, 1.f);
+    return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
+}
+// element i of an unrolled row loop: SPION_POLY of every 16 on the FMA pipe, the rest on the SFU
+__device__ __forceinline__ float ex2m(float x, int i) { return (i & 15) < SPION_POLY ? ex2_poly(x) : ex2(x); }  // max entries of one tile list (nblk <= 128)
 static constexpr float LOG2E = 1.4426950408889634f;
 static constexpr float LN2 = 0.6931471805599453f;
 
@@ -112,11 +165,8 @@ struct Tracer {
         if (p.trace && blockIdx.x == 0) base = p.trace + 16 + role * 2048;
     }
     __device__ __forceinline__ void ev(int id) {
-        if (base && n < 1024) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            base[2 * n] = (unsigned long long)id | ((unsigned long long)clock64() << 8);
-            base[2 * n + 1] = t;
+        if (base && n < 2048) {  // one 64-bit store: SM clock << 8 | event id
+            base[n] = (unsigned long long)id | ((unsigned long long)clock64() << 8);
             ++n;
         }
     }
@@ -322,9 +372,13 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(kv_full + st, STG);
-                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                        if (SPION_DBG_NOLOAD) {
+                            mbar_arrive(kv_full + st);
+                        } else {
+                            mbar_arrive_expect_tx(kv_full + st, STG);
+                            tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                            tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                        }
                     }
                     __syncwarp();
                     if (++st == NST) { st = 0; ph ^= 1; }
@@ -355,7 +409,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
                     if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
                         mma_commit(s_full + b);
                         if (sj == cnt - 1) mma_commit(q_empty + qb);
                     }
@@ -384,7 +438,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < B / 16; ++k)
-                        mma_bf16_ts(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
+                        MMA_TS(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
                     mma_commit(freeb + b);
                     mma_commit(kv_empty + pst);  // S(pj) (K) completed before P(pj) existed
                 }
@@ -443,7 +497,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 uint32_t packed[B / 2];
                 float alpha = 1.f;
                 bool rescale = false;
-                if (active) {
+                if (active && !SPION_DBG_NOSOFTMAX) {
                     float s[B];  // raw scores; the softmax scale is folded into the exponent
 #pragma unroll
                     for (int hh = 0; hh < B / 32; ++hh) {
@@ -453,9 +507,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
                         for (int i = 0; i < 32; ++i) s[hh * 32 + i] = v[i];
                     }
-                    float mx = s[0];
+                    float m4[4] = {s[0], s[1], s[2], s[3]};  // 4 independent chains (latency)
 #pragma unroll
-                    for (int i = 1; i < B; ++i) mx = fmaxf(mx, s[i]);
+                    for (int i = 4; i < B; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
+                    float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                     mx *= sl2;  // scale > 0: max commutes with the scaling (log2 domain)
                     if (m_run == -INFINITY) {
                         m_run = mx;
@@ -467,7 +522,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     float sum = 0.f;
 #pragma unroll
                     for (int i = 0; i < B; i += 2) {
-                        const float e0 = ex2(fmaf(s[i], sl2, -m_run)), e1 = ex2(fmaf(s[i + 1], sl2, -m_run));
+                        const float e0 = ex2m(fmaf(s[i], sl2, -m_run), i), e1 = ex2m(fmaf(s[i + 1], sl2, -m_run), i + 1);
                         sum += e0 + e1;
                         packed[i / 2] = pack_bf16(e0, e1);
                     }
@@ -561,14 +616,14 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 // block J: S, dP into one of NBUF TMEM buffer pairs -> dS = exp(S c - lse)(dP - D),
 // packed bf16 over S -> dQ += dS K_J (A from TMEM).  No atomics, no fp32 round trip.
 template <int B>
-__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DQ_MW), Cfg<B>::DQ_CTAS)
+__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DQ_MW, Cfg<B>::DQ_NSW), Cfg<B>::DQ_CTAS)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdQ, TcParams p) {
-    constexpr int NST = Cfg<B>::DQ_NST, NBUF = Cfg<B>::DQ_NBUF, MW = Cfg<B>::DQ_MW;
+    constexpr int NST = Cfg<B>::DQ_NST, NBUF = Cfg<B>::DQ_NBUF, MW = Cfg<B>::DQ_MW, NSW = Cfg<B>::DQ_NSW;
     constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
     constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
-    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3;
+    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
     constexpr uint32_t BUFW = 2 * B;  // S at b*BUFW, dP at b*BUFW + B
     constexpr uint32_t COL_DQ = NBUF * BUFW;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;
@@ -582,7 +637,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     uint8_t *sSched = sKV + NST * STG;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
     uint64_t *q_full = bars + 0, *q_empty = bars + 2, *o_full = bars + 4, *o_empty = bars + 5, *dq_full = bars + 6,
-             *s_full = bars + 7, *ds_full = s_full + NBUF, *freeb = ds_full + NBUF, *kv_full = freeb + NBUF,
+             *s_full = bars + 7, *ds_full = s_full + 2 * NBUF, *freeb = ds_full + NBUF, *kv_full = freeb + NBUF,
              *kv_empty = kv_full + NST;
     Sched sc = make_sched(sSched, kv_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
@@ -593,15 +648,18 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     if (threadIdx.x == 0) {
         // q_empty: the last MMA of the item, and the epilogue's TMA store of dQ (staged in the
         // same buffer) having read shared memory
-        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 2); }
-        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(ds_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, NSW + 1); }
+        // s_full[2b + w]: S, dP of buffer b ready for softmax warpgroup w (PP) — one barrier per
+        // (buffer, consumer) so every barrier has one in-order producer and one in-order consumer
+        for (int i = 0; i < 2 * NBUF; ++i) mbar_init(s_full + i, 1);
+        for (int i = 0; i < NBUF; ++i) { mbar_init(ds_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(o_full, 1);
         mbar_init(o_empty, 32 * MW);
         mbar_init(dq_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
         mbar_init(acc_empty, 32 * MW);
-        sched_init(sc, 3 + MW);
+        sched_init(sc, 2 + NSW + MW);
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DQ_COLS>(tmem_slot);
@@ -643,9 +701,13 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 for (int j = 0; j < cnt; ++j) {
                     mbar_wait(kv_empty + st, ph ^ 1);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(kv_full + st, STG);
-                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                        if (SPION_DBG_NOLOAD) {
+                            mbar_arrive(kv_full + st);
+                        } else {
+                            mbar_arrive_expect_tx(kv_full + st, STG);
+                            tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                            tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                        }
                     }
                     __syncwarp();
                     if (++st == NST) { st = 0; ph ^= 1; }
@@ -653,8 +715,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             }
             __syncwarp();
         }
-    } else if (warp == W_MMA) {
-        // S / dP issuer (converged warp, one elected lane issues), up to NBUF blocks ahead
+    } else if (warp == W_MMA || warp >= W_MMA3) {
+        // S / dP issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
+        // with NSW = NBUF, warp sw issues the blocks whose score buffer is sw
+        const int sw = warp == W_MMA ? 0 : warp - W_MMA3 + 1;
         int sst = 0, nq = 0;
         uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
@@ -670,23 +734,30 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
-                    mbar_wait(kv_full + sst, sph);
+                    if (NSW > 1 && (int)b != sw) {
+                        if (++sst == NST) { sst = 0; sph ^= 1; }
+                        continue;
+                    }
+                    // buffer first: its release implies every earlier block's stage arrived, so
+                    // the stage wait below can never see a phase from two uses back
                     if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                    mbar_wait(kv_full + sst, sph);
                     tc_fence_after();
                     const uint32_t cs = b * BUFW;
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
                     const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + sst * STG + KV_BYTES));
                     if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
-                        mma_commit(s_full + b);
-                        if (sj == cnt - 1) mma_commit(q_empty + qb);  // Q, dO no longer read
+                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
+                        mma_commit(s_full + 2 * b + (PP ? (sj & 1) : 0));
                     }
                     __syncwarp();
                     if (++sst == NST) { sst = 0; sph ^= 1; }
                 }
+                if (elect_one()) mma_commit(q_empty + qb);  // Q, dO no longer read by this warp's MMAs
+                __syncwarp();
                 g += cnt;
             }
             sched_release(sc, ks, true);
@@ -711,7 +782,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                     if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ts(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
+                            MMA_TS(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
                                         (pj > 0) || (k > 0));
                         mma_commit(freeb + b);
                         mma_commit(kv_empty + pst);
@@ -752,7 +823,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         const int wg = warp >> 2;              // warpgroup: alternate blocks (MW = 8); epilogue halves
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        uint32_t dq_ph = 0, g = 0;
+        uint32_t dq_ph = 0, g = 0, sph = 0;  // sph: phase bit per score buffer (this warpgroup's uses)
         int nq = 0;
         const float sl2 = p.scale_log2;
         for (int ks = 0;; ++ks) {
@@ -801,22 +872,24 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             for (int jj = (PP ? wg : 0); jj < cnt; jj += (PP ? 2 : 1)) {
                 const bool active = (msks[jj] >> slot) & 1;
                 const uint32_t gs = g + jj, sb = gs % NBUF;
-                mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dQ MMA that read sb before
+                // also implies the dQ MMA that read sb before
+                mbar_wait(s_full + 2 * sb + (PP ? wg : 0), PP ? (sph >> sb) & 1 : (gs / NBUF) & 1);
+                sph ^= 1u << sb;
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
 #pragma unroll
                 for (int hh = 0; hh < CPT / 32; ++hh) {
                     const uint32_t c32 = (PP ? 0 : wg * CPT) + hh * 32;  // 32-column chunk
                     uint32_t pk[16];
-                    if (active) {
+                    if (active && !SPION_DBG_NOSOFTMAX) {
                         float sv[32], dp[32];
                         tmem_ld32(tl + cs + c32, sv);
                         tmem_ld32(tl + cs + B + c32, dp);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
-                            const float p0 = ex2(fmaf(sv[i], sl2, nl2));
-                            const float p1 = ex2(fmaf(sv[i + 1], sl2, nl2));
+                            const float p0 = ex2m(fmaf(sv[i], sl2, nl2), i);
+                            const float p1 = ex2m(fmaf(sv[i + 1], sl2, nl2), i + 1);
                             pk[i / 2] = pack_bf16(p0 * (dp[i] - Dr), p1 * (dp[i + 1] - Dr));
                         }
                     } else {
@@ -865,14 +938,14 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 // blocks ahead of the softmax warps); P^T, dS^T packed over them feed dV += P^T dO_I,
 // dK += dS^T Q_I as A operands from tensor memory.
 template <int B>
-__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DKV_MW), Cfg<B>::DKV_CTAS)
+__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DKV_MW, Cfg<B>::DKV_NSW), Cfg<B>::DKV_CTAS)
 attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcParams p) {
-    constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF, MW = Cfg<B>::DKV_MW;
+    constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF, MW = Cfg<B>::DKV_MW, NSW = Cfg<B>::DKV_NSW;
     constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
     constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
-    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3;
+    constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
     constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
     constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;
     constexpr uint32_t TILE = B * 128;
@@ -883,27 +956,34 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sKV = smem;  // buffer kb: K at kb*32768, V at kb*32768 + 16384
+    constexpr bool SEP = Cfg<B>::DKV_SEP;
     uint8_t *sStage = smem + 65536;
-    uint8_t *sSched = sStage + NST * STAGE;
+    uint8_t *sOut = sStage + NST * STAGE;  // SEP: dK at +0, dV at +16384
+    uint8_t *sSched = sOut + (SEP ? 32768 : 0);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
     uint64_t *kv_full = bars + 0, *kv_empty = bars + 2, *acc_full = bars + 4, *s_full = bars + 5,
-             *p_full = s_full + NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
+             *p_full = s_full + 2 * NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
     Sched sc = make_sched(sSched, q_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
-    uint64_t *staged = q_empty + NST + 9;  // [2]: dK/dV of the item using K/V buffer kb staged
+    // [2]: dK/dV of the item using K/V buffer kb staged there; SEP: [0] staged in sOut, [1] the
+    // store has read sOut (out_free)
+    uint64_t *staged = q_empty + NST + 9;
     uint64_t *acc_empty = staged + 2;      // the epilogue has read the dK/dV accumulators
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         // kv_empty: the last S^T/dP^T MMA of the item, and the epilogue's TMA store of dK/dV
         // (staged in the same buffer) having read shared memory
-        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 2); }
-        for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, NSW + (SEP ? 0 : 1)); }
+        // s_full[2b + w]: S^T, dP^T of buffer b ready for softmax warpgroup w (PP) — one barrier
+        // per (buffer, consumer), so each has one in-order producer and one in-order consumer
+        for (int i = 0; i < 2 * NBUF; ++i) mbar_init(s_full + i, 1);
+        for (int i = 0; i < NBUF; ++i) { mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(acc_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
+        for (int i = 0; i < 2; ++i) mbar_init(staged + i, SEP && i == 1 ? 1 : 32 * MW);
         mbar_init(acc_empty, 32 * MW);
-        sched_init(sc, 3 + MW);
+        sched_init(sc, 2 + NSW + MW);
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
@@ -945,11 +1025,15 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     if (lane == 0) tr.ev(3);
                     uint8_t *stg = sStage + st * STAGE;
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
-                        tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
-                        tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
-                        bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
-                        bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                        if (SPION_DBG_NOLOAD) {
+                            mbar_arrive(q_full + st);
+                        } else {
+                            mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
+                            tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
+                            tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
+                            bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                            bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                        }
                     }
                     __syncwarp();
                     if (++st == NST) { st = 0; ph ^= 1; }
@@ -957,9 +1041,11 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             }
             __syncwarp();
         }
-    } else if (warp == W_MMA) {
-        // S^T / dP^T issuer (converged warp, one elected lane issues), up to NBUF blocks ahead
-        Tracer tr(p, 1);
+    } else if (warp == W_MMA || warp >= W_MMA3) {
+        // S^T / dP^T issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
+        // with NSW = NBUF, warp sw issues the blocks whose score buffer is sw
+        const int sw = warp == W_MMA ? 0 : warp - W_MMA3 + 1;
+        Tracer tr(p, sw == 0 ? 1 : 4 + sw);
         int sst = 0, nk = 0;
         uint32_t sph = 0, g = 0;
         for (int ks = 0;; ++ks) {
@@ -977,8 +1063,16 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
-                    mbar_wait(q_full + sst, sph);
+                    if (NSW > 1 && (int)b != sw) {
+                        if (++sst == NST) { sst = 0; sph ^= 1; }
+                        continue;
+                    }
+                    if (lane == 0) tr.ev(40);
+                    // buffer first: its release implies every earlier block's stage arrived, so
+                    // the stage wait below can never see a phase from two uses back
                     if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                    if (lane == 0) tr.ev(42);
+                    mbar_wait(q_full + sst, sph);
                     if (lane == 0) tr.ev(12);
                     tc_fence_after();
                     uint8_t *stg = sStage + sst * STAGE;
@@ -987,16 +1081,20 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
                     if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
+                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
-                        mma_commit(s_full + b);
-                        if (sj == cnt - 1) mma_commit(kv_empty + kb);  // K/V no longer read by this item
+                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
+                        tr.ev(43);
+                        mma_commit(s_full + 2 * b + (PP ? (sj & 1) : 0));
+                        tr.ev(41);
                     }
                     __syncwarp();
                     if (lane == 0) tr.ev(14);
                     if (++sst == NST) { sst = 0; sph ^= 1; }
                 }
+                // K/V no longer read by this warp's MMAs of the item (the same lane issued them)
+                if (elect_one()) mma_commit(kv_empty + kb);
+                __syncwarp();
                 g += cnt;
             }
             sched_release(sc, ks, true);
@@ -1016,6 +1114,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 ++na;
                 for (int pj = 0; pj < cnt; ++pj) {
                     const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
+                    if (lane == 0) tr.ev(30);
                     mbar_wait(p_full + b, u & 1);
                     if (lane == 0) tr.ev(13);
                     tc_fence_after();
@@ -1024,17 +1123,20 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
                     const uint32_t cs = b * BUFW;
                     if (elect_one()) {
+                        tr.ev(31);
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ts(tmem + COL_DV, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
+                            MMA_TS(tmem + COL_DV, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
                                         (pj > 0) || (k > 0));
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            mma_bf16_ts(tmem + COL_DK, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
+                            MMA_TS(tmem + COL_DK, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
                                         (pj > 0) || (k > 0));
+                        tr.ev(32);
                         mma_commit(freeb + b);
                         mma_commit(q_empty + pst);
                         if (pj == cnt - 1) mma_commit(acc_full);
+                        tr.ev(33);
                     }
                     __syncwarp();
                     if (lane == 0) tr.ev(15);
@@ -1052,7 +1154,18 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
             const int bh = h[1], t = h[2], cnt = h[3];
-            if (cnt > 0) {
+            if (cnt > 0 && SEP) {
+                mbar_wait(staged, ns & 1);
+                ++ns;
+                if (lane == 0) {
+                    tma_store_3d(&tmdK, sOut, 0, t * 128, bh);
+                    tma_store_3d(&tmdV, sOut + 16384, 0, t * 128, bh);
+                    bulk_commit();
+                    bulk_wait_read0();
+                    mbar_arrive(staged + 1);
+                }
+                __syncwarp();
+            } else if (cnt > 0) {
                 const int sb = ns & 1;
                 mbar_wait(staged + sb, (ns >> 1) & 1);
                 ++ns;
@@ -1073,7 +1186,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         const int wg = warp >> 2;              // warpgroup: alternate blocks (MW = 8); epilogue halves
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        uint32_t a_ph = 0, ph = 0, g = 0;
+        uint32_t a_ph = 0, ph = 0, g = 0, sph = 0;  // sph: phase bit per score buffer (this warpgroup's uses)
         int st = 0, nk = 0;
         const float sl2 = p.scale_log2;
         Tracer tr(p, 2 + (threadIdx.x == 128));
@@ -1104,11 +1217,15 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     continue;
                 }
                 const bool active = (msks[jj] >> slot) & 1;
-                mbar_wait(q_full + st, ph);  // lse_I, D_I
+                const uint32_t gs = g + jj, sb = gs % NBUF;
+                // also implies the dV/dK MMAs that read sb before
+                mbar_wait(s_full + 2 * sb + (PP ? wg : 0), PP ? (sph >> sb) & 1 : (gs / NBUF) & 1);
+                sph ^= 1u << sb;
+                // lse_I, D_I: after the S wait, whose MMA already waited this stage's load (so
+                // this parity wait can never see the stage's previous use)
+                mbar_wait(q_full + st, ph);
                 const float *snl2 = reinterpret_cast<const float *>(sStage + st * STAGE + 2 * TILE);
                 const float *sD = snl2 + 128;
-                const uint32_t gs = g + jj, sb = gs % NBUF;
-                mbar_wait(s_full + sb, (gs / NBUF) & 1);  // also implies the dV/dK MMAs that read sb before
                 if (trc) tr.ev(21);
                 tc_fence_after();
                 const uint32_t cs = sb * BUFW;
@@ -1116,7 +1233,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 for (int hh = 0; hh < CPT / 32; ++hh) {
                     const uint32_t c32 = (PP ? 0 : wg * CPT) + hh * 32;  // 32-column chunk
                     uint32_t pk[16], dk[16];
-                    if (active) {
+                    if (active && !SPION_DBG_NOSOFTMAX) {
                         float sv[32], dp[32], nl[32], dd[32];
                         tmem_ld32(tl + cs + c32, sv);
                         tmem_ld32(tl + cs + B + c32, dp);
@@ -1130,8 +1247,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
-                            const float p0 = ex2(fmaf(sv[i], sl2, nl[i]));
-                            const float p1 = ex2(fmaf(sv[i + 1], sl2, nl[i + 1]));
+                            const float p0 = ex2m(fmaf(sv[i], sl2, nl[i]), i);
+                            const float p1 = ex2m(fmaf(sv[i + 1], sl2, nl[i + 1]), i + 1);
                             pk[i / 2] = pack_bf16(p0, p1);
                             dk[i / 2] = pack_bf16(p0 * (dp[i] - dd[i]), p1 * (dp[i + 1] - dd[i + 1]));
                         }
@@ -1157,17 +1274,27 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             // then one TMA store per tile (coalesced; rows past L clipped)
             const int kb = nk & 1;
             ++nk;
-            uint8_t *sdK = sKV + kb * 32768, *sdV = sdK + 16384;
+            uint8_t *sdK = SEP ? sOut : sKV + kb * 32768, *sdV = sdK + 16384;
             if (MW == 8) {  // warpgroup 0 stages dK, warpgroup 1 stages dV
                 const uint32_t col = wg == 0 ? COL_DK : COL_DV;
                 uint8_t *dst = wg == 0 ? sdK : sdV;
                 const float f = wg == 0 ? p.scale : 1.f;
+                float v[64];
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    float v[32];
-                    tmem_ld32(tl + col + hh * 32, v);
+                    float w[32];
+                    tmem_ld32(tl + col + hh * 32, w);
                     tmem_ld_wait();
-                    stage_row_bf16(dst, r, v, f, hh);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[hh * 32 + i] = w[i];
+                }
+                if (SEP && nk > 1) mbar_wait(staged + 1, (nk - 2) & 1);  // the last store has read sOut
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    float w[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) w[i] = v[hh * 32 + i];
+                    stage_row_bf16(dst, r, w, f, hh);
                 }
             } else {
 #pragma unroll
@@ -1183,7 +1310,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             tc_fence_before();
             mbar_arrive(acc_empty);    // the next item's first dV/dK MMAs may overwrite the accumulators
             fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
-            mbar_arrive(staged + kb);
+            mbar_arrive(staged + (SEP ? 0 : kb));
             tc_fence_before();
             if (trc) tr.ev(24);
             g += cnt;
@@ -1290,7 +1417,9 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
 static const size_t SCHED_AREA = SCHED_BYTES + 1024;  // scheduler ring + mbarriers + TMEM slot
 template <int B> static size_t fwd_smem() { return 1024 + 32768 + Cfg<B>::FWD_NST * 2 * B * 128 + SCHED_AREA; }
 template <int B> static size_t dq_smem() { return 1024 + 81920 + Cfg<B>::DQ_NST * 2 * B * 128 + SCHED_AREA; }
-template <int B> static size_t dkv_smem() { return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + SCHED_AREA; }
+template <int B> static size_t dkv_smem() {
+    return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + (Cfg<B>::DKV_SEP ? 32768 : 0) + SCHED_AREA;
+}
 
 static int grid_for(const TcParams &p, int ctas) {
     const int64_t items = p.bh * p.ntiles;
@@ -1347,7 +1476,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     p.D = const_cast<float *>(a.D);
     p.nlse2 = a.nlse2;
     p.dQ = a.dQ;
-    attn_bwd_dq_tc_kernel<B><<<grid_for(p, Cfg<B>::DQ_CTAS), bwd_threads(Cfg<B>::DQ_MW), dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, mdq128, p);
+    attn_bwd_dq_tc_kernel<B><<<grid_for(p, Cfg<B>::DQ_CTAS), bwd_threads(Cfg<B>::DQ_MW, Cfg<B>::DQ_NSW), dq_smem<B>(), s>>>(mq128, mdo128, mo128, mkB, mvB, mdq128, p);
     SPION_LAUNCH_CHECK();
     // 2) dK, dV (column tiles)
     TcParams q = base_params(a, 2, Cfg<B>::DKV_CTAS);
@@ -1355,7 +1484,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     q.D = const_cast<float *>(a.D);
     q.dK = a.dK;
     q.dV = a.dV;
-    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), bwd_threads(Cfg<B>::DKV_MW), dkv_smem<B>(), s>>>(
+    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), bwd_threads(Cfg<B>::DKV_MW, Cfg<B>::DKV_NSW), dkv_smem<B>(), s>>>(
         mk128, mv128, mqB, mdoB, mdk128, mdv128, q);
     SPION_LAUNCH_CHECK();
     return SPION_OK;

@@ -4,7 +4,7 @@ o=gpurun_out/$tag; mkdir -p $o
 for v in "$@"; do
   if [ "$v" = base ]; then lib=""; else lib=build_variants/$v/libspion.so; fi
   for c in $cfgs; do
-    SPION_LIB=$lib timeout 300 python bench.py --config $c --no-cpu-baseline --e2e-steps 0 > $o/bench_${v}_$c.json 2> $o/bench_${v}_$c.err
+    SPION_LIB=$lib timeout 120 python bench.py --config $c --no-cpu-baseline --e2e-steps 0 > $o/bench_${v}_$c.json 2> $o/bench_${v}_$c.err
     python - <<PY
 import json
 try:

@@ -18,7 +18,18 @@ __global__ void k(int reps, long long *out, float *sink) {
             if (MODE == 0) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i])); }
             else if (MODE == 1) { asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u[i])); }
             else if (MODE == 2) { asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i])); }
-            else if (MODE == 4) {  // packed f32x2 poly exp2 on pairs
+            else if (MODE == 5) {  // cvt.rn.bf16x2.f32 (F2FP pack), independent chains
+                uint32_t v;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(v) : "f"(a[i]), "f"(__uint_as_float(u[i])));
+                u[i] = v ^ 0x1u;
+            } else if (MODE == 7) {  // one MUFU.EX2 + one F2FP per step
+                asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+                uint32_t v;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(v) : "f"(__uint_as_float(u[i])), "f"(__uint_as_float(u[i] + 1)));
+                u[i] = v ^ 0x1u;
+            } else if (MODE == 6) {  // FMUL + FADD pair (FP32 pipe reference)
+                a[i] = fmaf(a[i], 0.999f, -0.001f);
+            } else if (MODE == 4) {  // packed f32x2 poly exp2 on pairs
                 uint64_t x2, t2, j2, f2, p2;
                 float xa = a[i], xb = -a[i] * 0.5f;
                 asm("mov.b64 %0, {%1, %2};" : "=l"(x2) : "f"(xa), "f"(xb));
@@ -68,6 +79,9 @@ int main() {
     run<0>("ex2.approx.ftz.f32", 1);
     run<1>("ex2.approx.f16x2", 2);
     run<2>("ex2.approx.ftz.bf16x2", 2);
+    run<5>("cvt.rn.bf16x2.f32 (F2FP)", 2);
+    run<6>("FFMA", 1);
+    run<7>("MUFU.EX2 + F2FP pairs", 1);
     run<3>("poly3 exp2 (FMA pipe)", 1);
     run<4>("poly3 exp2 f32x2 (pairs)", 2);
     return 0;

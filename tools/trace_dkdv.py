@@ -1,9 +1,8 @@
-"""Debug: event trace of CTA 0 of the dK/dV kernel (SPION_TRACE=1).
+"""Debug: event trace of CTA 0 of the dK/dV kernel (SPION_TRACE=1); each event = SM clock << 8 | id.
 
-roles: 0 producer (1 item, 2 K/V issue, 3 Q stage issue), 1 MMA (10 item, 11 kv_full,
-12 S issue, 13 dV/dK issue), 2/3 softmax warp 0 / warp 4 lane 0 (20 item, 21 s_full,
-22 p arrive, 23 acc_full, 24 epilogue done)."""
-import ctypes, os, sys
+roles: 0 producer, 1 S^T/dP^T MMA warp, 2/3 softmax thread 0 / 128, 4 dV/dK MMA warp.
+Prints the median cycles between consecutive events of each role, and a raw window."""
+import collections, ctypes, os, sys
 os.environ["SPION_TRACE"] = "1"
 import numpy as np, torch
 sys.path.insert(0, ".")
@@ -23,53 +22,40 @@ torch.cuda.synchronize()
 lib = N.lib()
 lib.spion_debug_trace.restype = ctypes.c_int64
 R = 5
-buf = (ctypes.c_ulonglong * (R * 2048))()
-n = lib.spion_debug_trace(buf, R * 2048)
-a = np.array(buf[:n], dtype=np.uint64).reshape(R, 1024, 2)
+buf = (ctypes.c_ulonglong * (8 * 2048))()
+n = lib.spion_debug_trace(buf, 8 * 2048)
+a = np.array(buf[:n], dtype=np.uint64).reshape(8, 2048)
+names = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "S waits done",
+         13: "dVdK p_full done", 14: "S syncwarp done", 15: "dVdK syncwarp done", 20: "sm item", 21: "sm s_full",
+         22: "sm p arrive", 23: "sm acc_full", 24: "sm epi done", 30: "dVdK loop top", 31: "dVdK elect",
+         32: "dVdK MMAs issued", 33: "dVdK commits done", 40: "S loop top", 41: "S commits done", 42: "S q_full done",
+         43: "S MMAs issued"}
 evs = []
-names = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "M S issue", 13: "M dVdK issue", 14: "M S issued", 15: "M dVdK issued", 16: "m S0", 17: "m S4", 18: "m S8",
-         20: "S item", 21: "S s_full", 22: "S p arrive", 23: "S acc_full", 24: "S epi done"}
-clk = []
-mm = []
 for role in range(R):
-    for e, t in a[role]:
-        if t:
-            evs.append((int(t), int(e) & 255, role))
-            clk.append((int(t), int(e) >> 8))
-            if role == 1 and (int(e) & 255) in (16, 17, 18): mm.append((int(e) & 255, int(e) >> 8))
-clk.sort()
-mm.sort(key=lambda x: x[1])
-d1 = [b[1] - a[1] for a, b in zip(mm, mm[1:]) if a[0] == 16 and b[0] == 17]
-d2 = [b[1] - a[1] for a, b in zip(mm, mm[1:]) if a[0] == 17 and b[0] == 18]
-raw = sorted([(int(e) >> 8, int(e) & 255) for e, t in a[1] if t])
-import os
-if os.environ.get("RAW"):
-    for c, e in raw[200:260]: print("   clk", c - raw[0][0], names.get(e, e))
-if d1: print("issue cycles: first 4 SS MMAs median %d, next 4 median %d" % (sorted(d1)[len(d1) // 2], sorted(d2)[len(d2) // 2]))
-print("SM clock during the trace: %.0f MHz" % ((clk[-1][1] - clk[0][1]) / (clk[-1][0] - clk[0][0]) * 1e3))
+    for w in a[role]:
+        w = int(w)
+        if w:
+            evs.append((w >> 8, w & 255, role))
 evs.sort()
-t0 = evs[0][0]
-names0 = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "M S issue", 13: "M dVdK issue", 14: "M S issued", 16: "m S0", 17: "m S4", 18: "m S8", 15: "M dVdK issued",
-         20: "S item", 21: "S s_full", 22: "S p arrive", 23: "S acc_full", 24: "S epi done"}
-lim = int(sys.argv[2]) if len(sys.argv) > 2 else 120
-for t, e, r in evs[:lim]:
-    print(f"{(t - t0) / 1000:9.3f} us  r{r} {names.get(e, e)}")
-T = (evs[-1][0] - t0) / 1000
-def times(code, role=None):
-    return np.array([t for t, e, r in evs if e == code and (role is None or r == role)], dtype=np.int64)
-print("span us", T, "items", len(times(10)), "entries", len(times(12)))
-s21, s22 = times(21, 2), times(22, 2)
-m = min(len(s21), len(s22))
-print("softmax wg0: compute per entry us", np.mean(s22[:m] - s21[:m]) / 1000, " busy frac", np.sum(s22[:m] - s21[:m]) / 1000 / T)
-e23, e24 = times(23, 2), times(24, 2)
-m = min(len(e23), len(e24))
-print("epilogue us", np.mean(e24[:m] - e23[:m]) / 1000, " total", np.sum(e24[:m] - e23[:m]) / 1000)
-for a_, b_, nm in [(23, 25, "acc_full->staged"), (25, 26, "staged->barrier"), (26, 24, "barrier->done")]:
-    for role in (2, 3):
-        x, y = times(a_, role), times(b_, role)
-        m = min(len(x), len(y))
-        if m:
-            print(f"  r{role} {nm}: {np.mean(y[:m] - x[:m]) / 1000:.3f} us")
-# per item: acc_full wait duration (last p arrive -> acc_full)
-x, y = times(22, 2), times(23, 2)
-print("items", len(y))
+c0 = evs[0][0]
+for role in range(R):
+    ev = [(c, e) for c, e, r in evs if r == role]
+    dd = collections.defaultdict(list)
+    for (x0, e0), (x1, e1) in zip(ev, ev[1:]):
+        dd[(e0, e1)].append(x1 - x0)
+    print("role", role, "events", len(ev), "span", (ev[-1][0] - ev[0][0]) if ev else 0, "median cycles between consecutive events:")
+    for (e0, e1), vv in sorted(dd.items(), key=lambda kv: -len(kv[1]))[:10]:
+        if len(vv) > 10:
+            print("   %-20s -> %-20s n=%4d median %6d" % (names.get(e0, e0), names.get(e1, e1), len(vv), sorted(vv)[len(vv) // 2]))
+lo = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+for c, e, r in evs[lo:lo + 80]:
+    print(f"{c - c0:9d} r{r} {names.get(e, e)}")
+# gaps in the dV/dK warp's issue stream (role 4, event 15 = a block's dV/dK MMAs issued)
+iss = [c for c, e, r in evs if r == 4 and e == 15]
+items = [c for c, e, r in evs if r == 1 and e == 10]
+gaps = [(b - a, a - c0) for a, b in zip(iss, iss[1:])]
+print("dVdK issues", len(iss), "median gap", sorted(g for g, _ in gaps)[len(gaps) // 2], "sum of gaps > 2000:",
+      sum(g for g, _ in gaps if g > 2000), "of span", iss[-1] - iss[0])
+print("largest gaps (cycles, at):", sorted(gaps, reverse=True)[:12])
+print("item starts:", [c - c0 for c in items][:40])
+print("first/last event of the CTA:", evs[0][0] - c0, evs[-1][0] - c0)
