@@ -31,7 +31,7 @@ int64_t spion_launch_count(void) { return (int64_t)g_launches.load(); }
 SPION_API int64_t spion_debug_k2_trace(unsigned long long *host) {
     if (!spion::g_k2_trace) return 0;
     cudaDeviceSynchronize();
-    cudaMemcpy(host, spion::g_k2_trace, 8 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(host, spion::g_k2_trace, 16 * 8, cudaMemcpyDeviceToHost);
     return 8;
 }
 SPION_API int64_t spion_debug_trace(unsigned long long *host, int64_t cap) {

@@ -376,6 +376,7 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
         *reinterpret_cast<uint4 *>(sc.colw + c * 4) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     __syncthreads();
+    k2_stamp(a, 7);
     for (int r = tid; r < 2 * n; r += nthr)
         sc.cnt[r] = b_popc(b_load(r < n ? sc.flw + r * 4 : sc.colw + (r - n) * 4));
     __syncthreads();
@@ -386,23 +387,24 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
         *a.nnzb = nnzb;
         if (nnzb > a.nnzb_cap && a.flags) atomicOr(a.flags, FLAG_CAPACITY);
     }
+    k2_stamp(a, 8);
     for (int r = tid; r <= n; r += nthr) { a.brow_ptr[r] = sc.off[r]; a.bcol_ptr[r] = sc.off[n + 1 + r]; }
-    // ascending column (row) indices by scanning the set bits
-    for (int r = tid; r < 2 * n; r += nthr) {
+    // ascending column (row) indices: one warp per row (column), lane l owns bits [4l, 4l + 4)
+    const int lane = tid & 31;
+    for (int r = tid >> 5; r < 2 * n; r += nthr >> 5) {
         const bool row = r < n;
-        const Bits m = b_load(row ? sc.flw + r * 4 : sc.colw + (r - n) * 4);
-        int o = row ? sc.off[r] : sc.off[n + 1 + (r - n)];
+        const unsigned *w = row ? sc.flw + r * 4 : sc.colw + (r - n) * 4;
+        const unsigned nib = (w[lane >> 3] >> ((lane & 7) * 4)) & 15u;
+        int o = (row ? sc.off[r] : sc.off[n + 1 + (r - n)]) + warp_excl_scan_i32(__popc(nib), lane);
         int *dst = row ? a.bcol_idx : a.brow_idx;
-        for (int half = 0; half < 2; ++half) {
-            unsigned long long w = half ? m.hi : m.lo;
-            while (w) {
-                const int j = half * 64 + __ffsll((long long)w) - 1;
-                w &= w - 1;
-                if (o < a.nnzb_cap) dst[o] = j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((nib >> k) & 1u) {
+                if (o < a.nnzb_cap) dst[o] = 4 * lane + k;
                 ++o;
             }
-        }
     }
+    k2_stamp(a, 9);
     if (a.mask) {
         const int N = n * n;
         for (int i = tid; i < N; i += nthr) a.mask[i] = (uint8_t)b_get(sc.flw + (i / n) * 4, i % n);
@@ -413,6 +415,7 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
     const PlanLayout pl(n, a.block);
     int *plan = a.plan;
     __syncthreads();
+    k2_stamp(a, 10);
     for (int t = tid; t < 2 * pl.ntiles; t += nthr) {
         const bool fwd = t < pl.ntiles;
         const int tt = fwd ? t : t - pl.ntiles;
@@ -439,7 +442,10 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
         }
     }
     __syncthreads();
-    for (int t = tid; t < 2 * pl.ntiles; t += nthr) {
+    k2_stamp(a, 11);
+    // one warp per tile: rank in descending work order, then the union list with slot masks
+    // (lane l owns union bits [4l, 4l + 4))
+    for (int t = tid >> 5; t < 2 * pl.ntiles; t += nthr >> 5) {
         const bool fwd = t < pl.ntiles;
         const int tt = fwd ? t : t - pl.ntiles;
         const unsigned *src = fwd ? sc.flw : sc.colw;
@@ -448,30 +454,33 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
         const int *cnt = sc.cnt + (fwd ? 0 : pl.ntiles);
         const int c = cnt[tt];
         int rank = 0;
-        for (int v = 0; v < pl.ntiles; ++v) rank += (cnt[v] > c) || (cnt[v] == c && v < tt);
-        plan[(fwd ? pl.forder : pl.border) + rank] = tt;
-        Bits u{0ull, 0ull};
-        for (int s = 0; s < pl.S; ++s) {
-            const int r = tt * pl.S + s;
-            if (r < n) u = b_or(u, b_load(src + r * 4));
+        for (int v0 = 0; v0 < pl.ntiles; v0 += 32) {
+            const int v = v0 + lane;
+            const bool before = v < pl.ntiles && ((cnt[v] > c) || (cnt[v] == c && v < tt));
+            rank += __popc(__ballot_sync(0xffffffffu, before));
         }
-        int o = sc.off[(fwd ? 0 : pl.ntiles + 1) + tt];
+        if (lane == 0) plan[(fwd ? pl.forder : pl.border) + rank] = tt;
+        const int wsel = lane >> 3, sh = (lane & 7) * 4;
+        unsigned nib = 0;
+        for (int sl = 0; sl < pl.S; ++sl) {
+            const int r = tt * pl.S + sl;
+            if (r < n) nib |= (src[r * 4 + wsel] >> sh) & 15u;
+        }
+        int o = sc.off[(fwd ? 0 : pl.ntiles + 1) + tt] + warp_excl_scan_i32(__popc(nib), lane);
         int *col = plan + (fwd ? pl.fcol : pl.brow);
         int *msk = plan + (fwd ? pl.fmsk : pl.bmsk);
-        for (int half = 0; half < 2; ++half) {
-            unsigned long long w = half ? u.hi : u.lo;
-            while (w) {
-                const int j = half * 64 + __ffsll((long long)w) - 1;
-                w &= w - 1;
-                int m = 0;
-                for (int s = 0; s < pl.S; ++s) {
-                    const int r = tt * pl.S + s;
-                    if (r < n) m |= (int)b_get(src + r * 4, j) << s;
-                }
-                col[o] = j;
-                msk[o] = m;
-                ++o;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!((nib >> k) & 1u)) continue;
+            const int j = 4 * lane + k;
+            int m = 0;
+            for (int sl = 0; sl < pl.S; ++sl) {
+                const int r = tt * pl.S + sl;
+                if (r < n) m |= (int)((src[r * 4 + wsel] >> (sh + k)) & 1u) << sl;
             }
+            col[o] = j;
+            msk[o] = m;
+            ++o;
         }
     }
 }
@@ -566,7 +575,22 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
     //   That recurrence is a carry chain: with g = X & rt, p = rt the carries of g + p are
     //   C[c] = R[c-1] & rt[c-1] (the cells entered by a right edge); R = X | C.
     //   marked = (entered by an edge AND > t) (Alg. 4 l.5-7) OR diagonal (Alg. 3 l.9-10)
-    if (tid == 0) {
+    if (tid == 0 && n <= 64) {  // the same sweep on 64-bit rows (half the dependent ops)
+        const unsigned long long all = ~0ull >> (64 - n);
+        unsigned long long vis = 0ull, dn = 0ull, dg = 0ull;
+#pragma unroll 4
+        for (int r = 0; r < n; ++r) {
+            const unsigned long long rt = b_load(rtw + r * 4).lo, gt = b_load(gtw + r * 4).lo;
+            const unsigned long long E = (vis & dn) | ((vis & dg) << 1);
+            const unsigned long long X = E | (r == 0 ? all : 1ull);
+            const unsigned long long gg = X & rt;
+            const unsigned long long C = (gg + rt) ^ (gg ^ rt);
+            vis = X | C;
+            b_store(sc.flw + r * 4, Bits{((E | C) & gt) | (1ull << r), 0ull});
+            dn = b_load(dnw + r * 4).lo;
+            dg = b_load(dgw + r * 4).lo;
+        }
+    } else if (tid == 0) {
         const Bits all = b_ones(n);
         Bits vis{0ull, 0ull}, dn{0ull, 0ull}, dg{0ull, 0ull};
 #pragma unroll 4
