@@ -51,6 +51,19 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+# DRAM bytes per launch of each call from one `ncu --set full` capture (tools/ncu_traffic.py)
+TRAFFIC_FILE = "profiles/r1/ncu_traffic.json"
+
+
+def ncu_traffic(config, call):
+    try:
+        with open(os.path.join(ROOT, TRAFFIC_FILE)) as f:
+            v = json.load(f).get(config, {}).get(call)
+        return float(v) if v is not None else None
+    except (OSError, ValueError):
+        return None
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """Samples SM clock and throttle reasons via NVML while the timed region runs."""
@@ -297,8 +310,10 @@ def main():
     dom = max(ph_ms, key=ph_ms.get)
     t_dom = ph_ms[dom] * 1e-3
     gbs = alg[dom] / t_dom / 1e9
+    traffic = ncu_traffic(args.config, dom)
     roofline = {"kernel": f"spion_attn_{dom}" if dom != "pattern" else "spion_pattern", "bound": "hbm",
-                "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "traffic": None,
+                "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "traffic": traffic,
+                "traffic_source": TRAFFIC_FILE if traffic is not None else None,
                 "peak_source": peak_src, "alg_bytes_per_launch": alg[dom], "ms_per_launch": ph_ms[dom],
                 "useful_tflops": flops[dom] / t_dom / 1e12 if flops[dom] else 0.0}
     step_flops = accounting.useful_flops(B, d, nnzb, bh)

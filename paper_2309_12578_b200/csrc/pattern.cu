@@ -23,6 +23,9 @@
 namespace spion {
 
 // ---------------------------------------------------------------- K1
+#ifndef SPION_K1_CTAS  // split a block row's source rows across CTAs until the grid has this many
+#define SPION_K1_CTAS (4 * 148)
+#endif
 static constexpr int K1_WARPS = 8;
 static constexpr int K1_MAXP = 2;  // (target row, column) pairs per lane
 
@@ -47,7 +50,7 @@ static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
     g.JC = (n + n_cc - 1) / n_cc;
     g.n_cc = (n + g.JC - 1) / g.JC;
     int rs = 1;  // split the rows of a block row until the grid covers the GPU a few times
-    while (g.n_cc * n * rs < 4 * 148 && B / (2 * rs) >= 2 * K1_WARPS) rs *= 2;
+    while (g.n_cc * n * rs < SPION_K1_CTAS && B / (2 * rs) >= 2 * K1_WARPS) rs *= 2;
     g.RP = (B + rs - 1) / rs;
     return true;
 }
