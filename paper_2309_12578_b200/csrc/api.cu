@@ -37,7 +37,7 @@ SPION_API int64_t spion_debug_k2_trace(unsigned long long *host) {
 SPION_API int64_t spion_debug_trace(unsigned long long *host, int64_t cap) {
     if (!spion::g_trace_buf) return 0;
     cudaDeviceSynchronize();
-    int64_t n = 8 * 2048;  // 8 roles x 2048 events
+    int64_t n = 8 * 2048 + 4096;  // 8 roles x 2048 events, then [start, end] per CTA
     if (n > cap) n = cap;
     cudaMemcpy(host, spion::g_trace_buf + 16, n * 8, cudaMemcpyDeviceToHost);
     return n;

@@ -150,6 +150,7 @@ struct TcParams {
     int off_ptr, off_col, off_msk;  // plan word offsets (row tiles: fptr/fcol/fmsk, column tiles: bptr/brow/bmsk)
     int off_order;                  // tiles in descending work order
     int off_sched;                  // plan words [off_sched] item counter, [off_sched+1] done counter
+    int off_heavy;                  // plan word: number of heavy tiles (scheduled first)
     int G;                          // (batch, head) chunk of the scheduling order
     int S;                          // slots per tile
     unsigned long long *trace;      // optional event trace of CTA 0 (SPION_TRACE=1), else null
@@ -224,12 +225,23 @@ __device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcPar
         item = -1;
         if (lane == 0) h[0] = -1;
     } else {
-        const int per = p.G * p.ntiles;
-        const int c = item / per;
-        const int rem = item - c * per;
-        const int Gc = min(p.G, (int)p.bh - c * p.G);
-        const int kk = rem / Gc;
-        const int bh = c * p.G + (rem - kk * Gc);
+        // heavy tiles first for every (batch, head); then chunks of G (batch, head), each
+        // chunk's remaining tiles in descending work order (its K/V or Q/dO stay in L2)
+        const int nh = p.plan[p.off_heavy];
+        int kk, bh;
+        if (item < nh * (int)p.bh) {
+            kk = item / (int)p.bh;
+            bh = item - kk * (int)p.bh;
+        } else {
+            const int rest = item - nh * (int)p.bh;
+            const int per = p.G * (p.ntiles - nh);
+            const int c = rest / per;
+            const int rem = rest - c * per;
+            const int Gc = min(p.G, (int)p.bh - c * p.G);
+            const int k2 = rem / Gc;
+            bh = c * p.G + (rem - k2 * Gc);
+            kk = nh + k2;
+        }
         const int t = p.plan[p.off_order + kk];
         const int beg = p.plan[p.off_ptr + t], cnt = p.plan[p.off_ptr + t + 1] - beg;
         for (int e = lane; e < cnt; e += 32) {
@@ -262,7 +274,17 @@ __device__ __forceinline__ void sched_release(const Sched &sc, int k, bool whole
     }
 }
 
-__device__ __forceinline__ void sched_finish(const TcParams &p) {
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// SPION_TRACE: per-CTA [start, end] globaltimer after the role loops (load balance)
+__device__ __forceinline__ void sched_finish(const TcParams &p, unsigned long long t_start) {
+    if (p.trace && threadIdx.x == 0) {
+        p.trace[16 + 8 * 2048 + 2 * blockIdx.x] = t_start;
+        p.trace[16 + 8 * 2048 + 2 * blockIdx.x + 1] = gtimer();
+    }
     if (threadIdx.x == 0) {
         int *ctr = const_cast<int *>(p.plan) + p.off_sched;
         __threadfence();
@@ -347,6 +369,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const unsigned long long t_start = p.trace ? gtimer() : 0ull;
     const int nitems = (int)(p.bh * p.ntiles);
 
     if (warp == W_PROD) {
@@ -604,7 +627,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         }
     }
     __syncthreads();
-    sched_finish(p);
+    sched_finish(p, t_start);
     if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<Cfg<B>::FWD_COLS>(tmem);
@@ -667,6 +690,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const unsigned long long t_start = p.trace ? gtimer() : 0ull;
     const int nitems = (int)(p.bh * p.ntiles);
 
     if (warp == W_PROD) {
@@ -925,7 +949,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         }
     }
     __syncthreads();
-    sched_finish(p);
+    sched_finish(p, t_start);
     if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<Cfg<B>::DQ_COLS>(tmem);
@@ -991,6 +1015,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const unsigned long long t_start = p.trace ? gtimer() : 0ull;
     const int nitems = (int)(p.bh * p.ntiles);
 
     if (warp == W_PROD) {
@@ -1318,7 +1343,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         }
     }
     __syncthreads();
-    sched_finish(p);
+    sched_finish(p, t_start);
     if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc<Cfg<B>::DKV_COLS>(tmem);
@@ -1397,6 +1422,7 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     p.off_msk = (int)(rows ? pl.fmsk : pl.bmsk);
     p.off_order = (int)(rows ? pl.forder : pl.border);
     p.off_sched = 8 + 2 * which;
+    p.off_heavy = rows ? 5 : 6;
     const int grid = ctas * num_sms();
     int G = (2 * grid + pl.ntiles - 1) / pl.ntiles;
     if (G < 1) G = 1;
@@ -1406,8 +1432,8 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     static int want = -1;
     if (want < 0) want = getenv("SPION_TRACE") != nullptr;
     if (want) {
-        if (!trace_buf) cudaMalloc(&trace_buf, (16 + 8 * 2048) * 8);
-        cudaMemset(trace_buf, 0, (16 + 8 * 2048) * 8);
+        if (!trace_buf) cudaMalloc(&trace_buf, (16 + 8 * 2048 + 4096) * 8);
+        cudaMemset(trace_buf, 0, (16 + 8 * 2048 + 4096) * 8);
         p.trace = trace_buf;
         g_trace_buf = trace_buf;
     }

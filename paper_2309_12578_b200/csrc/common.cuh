@@ -91,6 +91,7 @@ __device__ __forceinline__ int warp_excl_scan_i32(int v, int lane) {
 struct PlanLayout {
     int n, S, ntiles;
     // header words: [0] n [1] S [2] ntiles [3] fwd entries [4] bwd entries
+    //               [5] heavy row tiles [6] heavy column tiles (prefixes of the work orders)
     //               [8] fwd item counter [9] fwd done [10] bwd item counter [11] bwd done
     size_t fptr, bptr, forder, border, fcol, fmsk, brow, bmsk, words;
     __host__ __device__ PlanLayout(int n_, int block) {

@@ -22,6 +22,9 @@
 
 namespace spion {
 
+#ifndef SPION_HEAVY_FIRST  // plan: tiles with > 2x the mean work scheduled first (attention tail)
+#define SPION_HEAVY_FIRST 1
+#endif
 // ---------------------------------------------------------------- K1
 #ifndef SPION_K1_CTAS  // split a block row's source rows across CTAs until the grid has this many
 #define SPION_K1_CTAS (4 * 148)
@@ -437,11 +440,25 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
             plan[pl.fptr + r] = sc.off[r];
             plan[pl.bptr + r] = sc.off[pl.ntiles + 1 + r];
         }
+        // heavy tiles (more than twice the mean work; e.g. the columns of vertical stripes): the
+        // attention kernels schedule these first for every (batch, head), so no long tile is left
+        // for the end of the launch (the load-balance tail)
+        int heavy[2];
+        for (int which = 0; which < 2; ++which) {
+            const int *c = sc.cnt + which * pl.ntiles;
+            const long long tot = sc.off[which * (pl.ntiles + 1) + pl.ntiles];
+            int hv = 0;
+            for (int t = tid; t < pl.ntiles; t += 32) hv += SPION_HEAVY_FIRST && (long long)c[t] * pl.ntiles > 2 * tot;
+            for (int o = 16; o > 0; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+            heavy[which] = hv;
+        }
         if (tid == 0) {
             plan[0] = n; plan[1] = pl.S; plan[2] = pl.ntiles;
             plan[3] = sc.off[pl.ntiles];
             plan[4] = sc.off[2 * pl.ntiles + 1];
             for (int w = 5; w < 16; ++w) plan[w] = 0;  // scheduler counters start at zero
+            plan[5] = heavy[0];  // heavy row tiles (a prefix of the descending work order)
+            plan[6] = heavy[1];  // heavy column tiles
         }
     }
     __syncthreads();
