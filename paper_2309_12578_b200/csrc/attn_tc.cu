@@ -542,14 +542,20 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         m_run = mx;
                         rescale = true;
                     }
-                    float sum = 0.f;
+                    // packed fp32x2: s * scale*log2(e) - m for two columns per FFMA2; two running sums
+                    const uint64_t sl22 = f2pack(sl2, sl2), nm2 = f2pack(-m_run, -m_run);
+                    uint64_t sum2 = 0ull;
 #pragma unroll
                     for (int i = 0; i < B; i += 2) {
-                        const float e0 = ex2m(fmaf(s[i], sl2, -m_run), i), e1 = ex2m(fmaf(s[i + 1], sl2, -m_run), i + 1);
-                        sum += e0 + e1;
+                        float a0, a1;
+                        f2unpack(ffma2(f2pack(s[i], s[i + 1]), sl22, nm2), a0, a1);
+                        const float e0 = ex2m(a0, i), e1 = ex2m(a1, i + 1);
+                        sum2 = fadd2(sum2, f2pack(e0, e1));
                         packed[i / 2] = pack_bf16(e0, e1);
                     }
-                    l_run = l_run * alpha + sum;
+                    float s0, s1;
+                    f2unpack(sum2, s0, s1);
+                    l_run = l_run * alpha + (s0 + s1);
                 } else {
 #pragma unroll
                     for (int i = 0; i < B / 2; ++i) packed[i] = 0u;
@@ -910,11 +916,14 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         tmem_ld32(tl + cs + c32, sv);
                         tmem_ld32(tl + cs + B + c32, dp);
                         tmem_ld_wait();
+                        const uint64_t sl22 = f2pack(sl2, sl2), nl22 = f2pack(nl2, nl2), D2 = f2pack(Dr, Dr);
 #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float p0 = ex2m(fmaf(sv[i], sl2, nl2), i);
-                            const float p1 = ex2m(fmaf(sv[i + 1], sl2, nl2), i + 1);
-                            pk[i / 2] = pack_bf16(p0 * (dp[i] - Dr), p1 * (dp[i + 1] - Dr));
+                        for (int i = 0; i < 32; i += 2) {  // packed fp32x2 (FFMA2 / FADD2 / FMUL2)
+                            float a0, a1, d0, d1;
+                            f2unpack(ffma2(f2pack(sv[i], sv[i + 1]), sl22, nl22), a0, a1);
+                            const float p0 = ex2m(a0, i), p1 = ex2m(a1, i + 1);
+                            f2unpack(fmul2(f2pack(p0, p1), fsub2(f2pack(dp[i], dp[i + 1]), D2)), d0, d1);
+                            pk[i / 2] = pack_bf16(d0, d1);
                         }
                     } else {
 #pragma unroll
@@ -1270,12 +1279,15 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                             dd[4 * i] = b.x; dd[4 * i + 1] = b.y; dd[4 * i + 2] = b.z; dd[4 * i + 3] = b.w;
                         }
                         tmem_ld_wait();
+                        const uint64_t sl22 = f2pack(sl2, sl2);
 #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float p0 = ex2m(fmaf(sv[i], sl2, nl[i]), i);
-                            const float p1 = ex2m(fmaf(sv[i + 1], sl2, nl[i + 1]), i + 1);
+                        for (int i = 0; i < 32; i += 2) {  // packed fp32x2 (FFMA2 / FADD2 / FMUL2)
+                            float a0, a1, d0, d1;
+                            f2unpack(ffma2(f2pack(sv[i], sv[i + 1]), sl22, f2pack(nl[i], nl[i + 1])), a0, a1);
+                            const float p0 = ex2m(a0, i), p1 = ex2m(a1, i + 1);
                             pk[i / 2] = pack_bf16(p0, p1);
-                            dk[i / 2] = pack_bf16(p0 * (dp[i] - dd[i]), p1 * (dp[i + 1] - dd[i + 1]));
+                            f2unpack(fmul2(f2pack(p0, p1), fsub2(f2pack(dp[i], dp[i + 1]), f2pack(dd[i], dd[i + 1]))), d0, d1);
+                            dk[i / 2] = pack_bf16(d0, d1);
                         }
                     } else {
 #pragma unroll
