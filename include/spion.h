@@ -179,7 +179,13 @@ SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, cons
  * Tensors are contiguous [bh][L][d] (stride_l = d).  Host buffers should be
  * pinned for asynchronous copies.  dev_arena: caller-owned device memory of
  * >= spion_step_arena_bytes(...) bytes.  Synchronises `stream` and returns
- * nnzb in *nnzb_host (may be NULL). */
+ * nnzb in *nnzb_host (may be NULL).
+ * The (batch, head) range is processed in up to 8 contiguous chunks, pipelined:
+ * the H2D copy of chunk c+1, the attention of chunk c (on `stream`) and the D2H
+ * copy of chunk c-1 overlap, on two copy streams the library creates once per
+ * device and host thread (with their events: the ABI's only internal state).
+ * Results are identical to the unchunked device calls (every (batch, head) is
+ * computed independently and deterministically). */
 SPION_API size_t spion_step_arena_bytes(int64_t bh, int32_t L, int32_t d, int32_t block, spion_dtype dt);
 SPION_API spion_status spion_step_host(const float *scores_host, const void *Q_host, const void *K_host,
                              const void *V_host, const void *dO_host, void *O_host, float *lse_host,

@@ -275,6 +275,15 @@ struct Arena {
         plan, total;
 };
 
+// spion_step_host pipelines the step over C contiguous (batch, head) chunks: the H2D copy of
+// chunk c+1, the attention of chunk c and the D2H copy of chunk c-1 overlap (copy engines in
+// both directions and the SMs busy at once)
+static int step_chunks(int64_t bh) {
+    for (int C : {8, 4, 2})
+        if (bh % C == 0 && bh / C >= 8) return C;
+    return 1;
+}
+
 static Arena arena_layout(int64_t bh, int32_t L, int32_t d, int32_t block, spion_dtype dt) {
     Arena A;
     const size_t elt = dt == SPION_BF16 ? 2 : 4;
@@ -293,7 +302,8 @@ static Arena arena_layout(int64_t bh, int32_t L, int32_t d, int32_t block, spion
     A.dK = take(t);
     A.dV = take(t);
     A.pws = take(pattern_ws_bytes(L, block));
-    A.aws = take(spion_attn_workspace_bytes(bh, L, d, dt));
+    const int C = step_chunks(bh);
+    A.aws = take((size_t)C * spion_attn_workspace_bytes(bh / C, L, d, dt));  // one per bh chunk
     A.brow_ptr = take((size_t)(n + 1) * 4);
     A.bcol_idx = take((size_t)n * n * 4);
     A.bcol_ptr = take((size_t)(n + 1) * 4);
@@ -324,11 +334,52 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
     const size_t elt = dt == SPION_BF16 ? 2 : 4;
     const size_t t = (size_t)bh * L * d * elt;
     const int n = L / block;
-    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.scores, scores_host, (size_t)L * L * 4, cudaMemcpyHostToDevice, s));
-    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.Q, Q_host, t, cudaMemcpyHostToDevice, s));
-    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.K, K_host, t, cudaMemcpyHostToDevice, s));
-    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.V, V_host, t, cudaMemcpyHostToDevice, s));
-    SPION_CUDA_TRY(cudaMemcpyAsync(base + A.dO, dO_host, t, cudaMemcpyHostToDevice, s));
+    const int C = step_chunks(bh);
+    const int64_t bhc = bh / C;
+    const size_t tc = t / C, lc = (size_t)bhc * L * 4, wsc = spion_attn_workspace_bytes(bhc, L, d, dt);
+    // copy streams and events: created once per device and thread (the ABI's only state)
+    constexpr int MAXC = 8;
+    struct Pipe {
+        int dev = -1;
+        cudaStream_t h2d = nullptr, d2h = nullptr;
+        cudaEvent_t start, scores, in[MAXC], out[MAXC], done;
+    };
+    static thread_local Pipe P;
+    int dev = 0;
+    SPION_CUDA_TRY(cudaGetDevice(&dev));
+    if (P.dev != dev) {
+        SPION_CUDA_TRY(cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking));
+        SPION_CUDA_TRY(cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking));
+        SPION_CUDA_TRY(cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming));
+        SPION_CUDA_TRY(cudaEventCreateWithFlags(&P.scores, cudaEventDisableTiming));
+        SPION_CUDA_TRY(cudaEventCreateWithFlags(&P.done, cudaEventDisableTiming));
+        for (int c = 0; c < MAXC; ++c) {
+            SPION_CUDA_TRY(cudaEventCreateWithFlags(&P.in[c], cudaEventDisableTiming));
+            SPION_CUDA_TRY(cudaEventCreateWithFlags(&P.out[c], cudaEventDisableTiming));
+        }
+        P.dev = dev;
+    }
+    auto H2D = [&](size_t off, const void *src, size_t bytes) {
+        return cudaMemcpyAsync(base + off, src, bytes, cudaMemcpyHostToDevice, P.h2d);
+    };
+    auto D2H = [&](void *dst, size_t off, size_t bytes) {
+        return cudaMemcpyAsync(dst, base + off, bytes, cudaMemcpyDeviceToHost, P.d2h);
+    };
+    // everything earlier on the caller's stream first
+    SPION_CUDA_TRY(cudaEventRecord(P.start, s));
+    SPION_CUDA_TRY(cudaStreamWaitEvent(P.h2d, P.start, 0));
+    SPION_CUDA_TRY(cudaStreamWaitEvent(P.d2h, P.start, 0));
+    SPION_CUDA_TRY(H2D(A.scores, scores_host, (size_t)L * L * 4));
+    SPION_CUDA_TRY(cudaEventRecord(P.scores, P.h2d));
+    for (int c = 0; c < C; ++c) {
+        const char *q = static_cast<const char *>(Q_host), *k = static_cast<const char *>(K_host);
+        const char *v = static_cast<const char *>(V_host), *g = static_cast<const char *>(dO_host);
+        SPION_CUDA_TRY(H2D(A.Q + c * tc, q + c * tc, tc));
+        SPION_CUDA_TRY(H2D(A.K + c * tc, k + c * tc, tc));
+        SPION_CUDA_TRY(H2D(A.V + c * tc, v + c * tc, tc));
+        SPION_CUDA_TRY(H2D(A.dO + c * tc, g + c * tc, tc));
+        SPION_CUDA_TRY(cudaEventRecord(P.in[c], P.h2d));
+    }
     spion_bsr bsr;
     memset(&bsr, 0, sizeof(bsr));
     bsr.nnzb_cap = n * n;
@@ -340,22 +391,31 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
     bsr.nnzb = reinterpret_cast<int32_t *>(base + A.nnzb);
     bsr.plan = base + A.plan;
     bsr.plan_bytes = spion_bsr_plan_bytes(L, block);
+    SPION_CUDA_TRY(cudaStreamWaitEvent(s, P.scores, 0));
     spion_status st = spion_pattern(reinterpret_cast<const float *>(base + A.scores), L, block, filter, threshold,
                                     kind, base + A.pws, pattern_ws_bytes(L, block), &bsr, nullptr, stream);
     if (st) return st;
-    st = spion_attn_fwd(base + A.Q, base + A.K, base + A.V, base + A.O, reinterpret_cast<float *>(base + A.lse), bh,
-                        L, d, (int64_t)L * d, d, dt, &bsr, mode, scale, stream);
-    if (st) return st;
-    st = spion_attn_bwd(base + A.Q, base + A.K, base + A.V, base + A.O, base + A.dO,
-                        reinterpret_cast<const float *>(base + A.lse), base + A.dQ, base + A.dK, base + A.dV, bh, L,
-                        d, (int64_t)L * d, d, dt, &bsr, mode, scale, base + A.aws,
-                        spion_attn_workspace_bytes(bh, L, d, dt), stream);
-    if (st) return st;
-    if (O_host) SPION_CUDA_TRY(cudaMemcpyAsync(O_host, base + A.O, t, cudaMemcpyDeviceToHost, s));
-    if (lse_host) SPION_CUDA_TRY(cudaMemcpyAsync(lse_host, base + A.lse, (size_t)bh * L * 4, cudaMemcpyDeviceToHost, s));
-    if (dQ_host) SPION_CUDA_TRY(cudaMemcpyAsync(dQ_host, base + A.dQ, t, cudaMemcpyDeviceToHost, s));
-    if (dK_host) SPION_CUDA_TRY(cudaMemcpyAsync(dK_host, base + A.dK, t, cudaMemcpyDeviceToHost, s));
-    if (dV_host) SPION_CUDA_TRY(cudaMemcpyAsync(dV_host, base + A.dV, t, cudaMemcpyDeviceToHost, s));
+    for (int c = 0; c < C; ++c) {
+        const size_t o = c * tc;
+        float *lse = reinterpret_cast<float *>(base + A.lse + c * lc);
+        SPION_CUDA_TRY(cudaStreamWaitEvent(s, P.in[c], 0));
+        st = spion_attn_fwd(base + A.Q + o, base + A.K + o, base + A.V + o, base + A.O + o, lse, bhc, L, d,
+                            (int64_t)L * d, d, dt, &bsr, mode, scale, stream);
+        if (st) return st;
+        st = spion_attn_bwd(base + A.Q + o, base + A.K + o, base + A.V + o, base + A.O + o, base + A.dO + o, lse,
+                            base + A.dQ + o, base + A.dK + o, base + A.dV + o, bhc, L, d, (int64_t)L * d, d, dt, &bsr,
+                            mode, scale, base + A.aws + c * wsc, wsc, stream);
+        if (st) return st;
+        SPION_CUDA_TRY(cudaEventRecord(P.out[c], s));
+        SPION_CUDA_TRY(cudaStreamWaitEvent(P.d2h, P.out[c], 0));
+        if (O_host) SPION_CUDA_TRY(D2H(static_cast<char *>(O_host) + o, A.O + o, tc));
+        if (lse_host) SPION_CUDA_TRY(D2H(reinterpret_cast<char *>(lse_host) + c * lc, A.lse + c * lc, lc));
+        if (dQ_host) SPION_CUDA_TRY(D2H(static_cast<char *>(dQ_host) + o, A.dQ + o, tc));
+        if (dK_host) SPION_CUDA_TRY(D2H(static_cast<char *>(dK_host) + o, A.dK + o, tc));
+        if (dV_host) SPION_CUDA_TRY(D2H(static_cast<char *>(dV_host) + o, A.dV + o, tc));
+    }
+    SPION_CUDA_TRY(cudaEventRecord(P.done, P.d2h));
+    SPION_CUDA_TRY(cudaStreamWaitEvent(s, P.done, 0));
     int32_t nnzb = 0;
     SPION_CUDA_TRY(cudaMemcpyAsync(&nnzb, bsr.nnzb, 4, cudaMemcpyDeviceToHost, s));
     int flags = 0;

@@ -178,3 +178,38 @@ def test_full_size_sampled(cfg):
         assert np.isfinite(x[np.isfinite(x) | ~np.isinf(x)]).all()
     _compare(outs, q, k, v, do, fl, B, "paper", 1 / math.sqrt(d), [0, bh // 3, bh - 1], 2e-2, norm_tol=1e-2,
              lse_tol=1e-3)
+
+
+def test_step_host_matches_device_calls():
+    """spion_step_host (pipelined over (batch, head) chunks, host buffers) gives the same bytes as
+    spion_pattern + spion_attn_fwd + spion_attn_bwd on device buffers."""
+    import ctypes
+
+    spion = _spion()
+    from paper_2309_12578_b200 import _native as N
+
+    L, B, bh, d = 1024, 32, 16, 64
+    A = synth.lra_scores(L, B, seed=5)
+    q, k, v, do = synth.qkvdo(bh, L, d, seed=77, dtype=torch.bfloat16)
+    scale = 1 / math.sqrt(d)
+    bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
+    qd, kd, vd, dod = (x.to(DEV) for x in (q, k, v, do))
+    o, lse = spion.attn_fwd(qd, kd, vd, bp, "paper", scale)
+    dq, dk, dv = spion.attn_bwd(qd, kd, vd, o, dod, lse, bp, "paper", scale)
+    torch.cuda.synchronize()
+    lib = N.lib()
+    hA = A.pin_memory()
+    hq, hk, hv, hdo = (x.pin_memory() for x in (q, k, v, do))
+    ho, hdq, hdk, hdv = (torch.empty_like(hq).pin_memory() for _ in range(4))
+    hlse = torch.empty((bh, L), dtype=torch.float32).pin_memory()
+    nb = lib.spion_step_arena_bytes(bh, L, d, B, N.BF16)
+    arena = torch.empty(nb, dtype=torch.uint8, device=DEV)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    nnz = ctypes.c_int32(0)
+    st = lib.spion_step_host(P(hA), P(hq), P(hk), P(hv), P(hdo), P(ho), P(hlse), P(hdq), P(hdk), P(hdv), bh, L, d, B,
+                             31, 75.0, N.THRESH["linear"], N.BF16, N.SOFTMAX["paper"], scale, P(arena), nb,
+                             ctypes.byref(nnz), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    N.check(st, "spion_step_host")
+    assert nnz.value == bp.nnzb
+    for got, want in ((ho, o), (hlse, lse), (hdq, dq), (hdk, dk), (hdv, dv)):
+        assert torch.equal(got, want.cpu())
