@@ -54,14 +54,8 @@
 #ifndef SPION_DBG_NOSOFTMAX
 #define SPION_DBG_NOSOFTMAX 0
 #endif
-#ifndef SPION_SEPOUT  // output staging buffers separate from the per-item input tiles
-#define SPION_SEPOUT 0
-#endif
 #ifndef SPION_NSW  // 1: one S-MMA warp per buffer where one CTA owns the SM (0: a single S-MMA warp)
 #define SPION_NSW 0
-#endif
-#ifndef SPION_DKV_NBUF  // override of the dK/dV kernel's S^T/dP^T buffer count (0 = as many as fit)
-#define SPION_DKV_NBUF 0
 #endif
 #ifndef SPION_DBG_NOLOAD  // per-block operand tiles not loaded
 #define SPION_DBG_NOLOAD 0
@@ -97,11 +91,8 @@ template <int B> struct Cfg {
     static constexpr int DQ_NBUF = (DQ_COLS - 64) / (2 * B);   // S+dP buffers + dQ
     static constexpr int DQ_NST = B == 32 ? 3 : 8;             // K_J + V_J per stage
     static constexpr int DKV_CTAS = B == 32 ? 2 : 1, DKV_COLS = 512 / DKV_CTAS;
-    static constexpr int DKV_NBUF = SPION_DKV_NBUF > 0 ? SPION_DKV_NBUF : (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
-    // dK/dV staged for the TMA store in their own buffer (not over the item's K/V tiles), so
-    // the next-but-one item's K/V load need not wait for this item's store (one CTA per SM only)
-    static constexpr bool DKV_SEP = DKV_CTAS == 1 && SPION_SEPOUT;
-    static constexpr int DKV_NST = B == 32 ? 4 : (DKV_SEP ? 7 : 9);  // Q_I + dO_I + lse_I + D_I per stage
+    static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
+    static constexpr int DKV_NST = B == 32 ? 4 : 9;               // Q_I + dO_I + lse_I + D_I per stage
     // softmax warps of the backward kernels: two warpgroups (each takes half of a block's
     // columns) where one CTA owns the SM, one warpgroup where two CTAs share it
     static constexpr int DQ_MW = DQ_CTAS == 1 ? 8 : 4, DKV_MW = DKV_CTAS == 1 ? 8 : 4;
@@ -112,7 +103,7 @@ template <int B> struct Cfg {
     // commits, reconvergence) is not the limit, and every buffer's uses (and every ring stage's,
     // NST % NBUF == 0) stay in order within one warp, as mbarrier parity waits require
     static constexpr int DQ_NSW = DQ_CTAS == 1 && SPION_NSW ? DQ_NBUF : 1;
-    static constexpr int DKV_NSW = DKV_CTAS == 1 && SPION_NSW ? DKV_NBUF : 1;
+    static constexpr int DKV_NSW = 1;
     static_assert(FWD_NST >= FWD_NBUF && DQ_NST >= DQ_NBUF && DKV_NST >= DKV_NBUF, "ring shallower than look-ahead");
 };
 static constexpr int SCHED_CAP = 128;
@@ -989,32 +980,28 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sKV = smem;  // buffer kb: K at kb*32768, V at kb*32768 + 16384
-    constexpr bool SEP = Cfg<B>::DKV_SEP;
     uint8_t *sStage = smem + 65536;
-    uint8_t *sOut = sStage + NST * STAGE;  // SEP: dK at +0, dV at +16384
-    uint8_t *sSched = sOut + (SEP ? 32768 : 0);
+    uint8_t *sSched = sStage + NST * STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
     uint64_t *kv_full = bars + 0, *kv_empty = bars + 2, *acc_full = bars + 4, *s_full = bars + 5,
              *p_full = s_full + 2 * NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
     Sched sc = make_sched(sSched, q_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
-    // [2]: dK/dV of the item using K/V buffer kb staged there; SEP: [0] staged in sOut, [1] the
-    // store has read sOut (out_free)
-    uint64_t *staged = q_empty + NST + 9;
+    uint64_t *staged = q_empty + NST + 9;  // [2]: dK/dV of the item using K/V buffer kb staged there
     uint64_t *acc_empty = staged + 2;      // the epilogue has read the dK/dV accumulators
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         // kv_empty: the last S^T/dP^T MMA of the item, and the epilogue's TMA store of dK/dV
         // (staged in the same buffer) having read shared memory
-        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, NSW + (SEP ? 0 : 1)); }
+        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, NSW + 1); }
         // s_full[2b + w]: S^T, dP^T of buffer b ready for softmax warpgroup w (PP) — one barrier
         // per (buffer, consumer), so each has one in-order producer and one in-order consumer
         for (int i = 0; i < 2 * NBUF; ++i) mbar_init(s_full + i, 1);
         for (int i = 0; i < NBUF; ++i) { mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(acc_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        for (int i = 0; i < 2; ++i) mbar_init(staged + i, SEP && i == 1 ? 1 : 32 * MW);
+        for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
         mbar_init(acc_empty, 32 * MW);
         sched_init(sc, 2 + NSW + MW);
         fence_barrier_init();
@@ -1188,18 +1175,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
             const int bh = h[1], t = h[2], cnt = h[3];
-            if (cnt > 0 && SEP) {
-                mbar_wait(staged, ns & 1);
-                ++ns;
-                if (lane == 0) {
-                    tma_store_3d(&tmdK, sOut, 0, t * 128, bh);
-                    tma_store_3d(&tmdV, sOut + 16384, 0, t * 128, bh);
-                    bulk_commit();
-                    bulk_wait_read0();
-                    mbar_arrive(staged + 1);
-                }
-                __syncwarp();
-            } else if (cnt > 0) {
+            if (cnt > 0) {
                 const int sb = ns & 1;
                 mbar_wait(staged + sb, (ns >> 1) & 1);
                 ++ns;
@@ -1311,26 +1287,16 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             // then one TMA store per tile (coalesced; rows past L clipped)
             const int kb = nk & 1;
             ++nk;
-            uint8_t *sdK = SEP ? sOut : sKV + kb * 32768, *sdV = sdK + 16384;
+            uint8_t *sdK = sKV + kb * 32768, *sdV = sdK + 16384;
             if (MW == 8) {  // warpgroup 0 stages dK, warpgroup 1 stages dV
                 const uint32_t col = wg == 0 ? COL_DK : COL_DV;
                 uint8_t *dst = wg == 0 ? sdK : sdV;
                 const float f = wg == 0 ? p.scale : 1.f;
-                float v[64];
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     float w[32];
                     tmem_ld32(tl + col + hh * 32, w);
                     tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[hh * 32 + i] = w[i];
-                }
-                if (SEP && nk > 1) mbar_wait(staged + 1, (nk - 2) & 1);  // the last store has read sOut
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    float w[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) w[i] = v[hh * 32 + i];
                     stage_row_bf16(dst, r, w, f, hh);
                 }
             } else {
@@ -1347,7 +1313,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             tc_fence_before();
             mbar_arrive(acc_empty);    // the next item's first dV/dK MMAs may overwrite the accumulators
             fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
-            mbar_arrive(staged + (SEP ? 0 : kb));
+            mbar_arrive(staged + kb);
             tc_fence_before();
             if (trc) tr.ev(24);
             g += cnt;
@@ -1455,9 +1421,7 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
 static const size_t SCHED_AREA = SCHED_BYTES + 1024;  // scheduler ring + mbarriers + TMEM slot
 template <int B> static size_t fwd_smem() { return 1024 + 32768 + Cfg<B>::FWD_NST * 2 * B * 128 + SCHED_AREA; }
 template <int B> static size_t dq_smem() { return 1024 + 81920 + Cfg<B>::DQ_NST * 2 * B * 128 + SCHED_AREA; }
-template <int B> static size_t dkv_smem() {
-    return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + (Cfg<B>::DKV_SEP ? 32768 : 0) + SCHED_AREA;
-}
+template <int B> static size_t dkv_smem() { return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + SCHED_AREA; }
 
 static int grid_for(const TcParams &p, int ctas) {
     const int64_t items = p.bh * p.ntiles;
