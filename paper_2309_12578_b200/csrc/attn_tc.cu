@@ -54,6 +54,9 @@
 #ifndef SPION_DBG_NOSOFTMAX
 #define SPION_DBG_NOSOFTMAX 0
 #endif
+#ifndef SPION_HEAVY_AHEAD  // heavy tiles are scheduled this many (batch, head) chunks ahead
+#define SPION_HEAVY_AHEAD 2
+#endif
 #ifndef SPION_NSW  // 1: one S-MMA warp per buffer where one CTA owns the SM (0: a single S-MMA warp)
 #define SPION_NSW 0
 #endif
@@ -216,23 +219,29 @@ __device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcPar
         item = -1;
         if (lane == 0) h[0] = -1;
     } else {
-        // heavy tiles first for every (batch, head); then chunks of G (batch, head), each
-        // chunk's remaining tiles in descending work order (its K/V or Q/dO stay in L2)
+        // chunks of G (batch, head), each chunk's tiles in descending work order (its K/V or
+        // Q/dO stay in L2), with the heavy tiles (> 2x the mean work) of chunk c+A handed out
+        // before the light tiles of chunk c (A = SPION_HEAVY_AHEAD): long tiles start A chunks
+        // early, so none is left for the end of the launch, while the L2 working set stays
+        // A + 1 chunks.  Block order (A = 1): H0, H1, L0, H2, L1, ..., H(C-1), L(C-2), L(C-1)
         const int nh = p.plan[p.off_heavy];
-        int kk, bh;
-        if (item < nh * (int)p.bh) {
-            kk = item / (int)p.bh;
-            bh = item - kk * (int)p.bh;
-        } else {
-            const int rest = item - nh * (int)p.bh;
-            const int per = p.G * (p.ntiles - nh);
-            const int c = rest / per;
-            const int rem = rest - c * per;
-            const int Gc = min(p.G, (int)p.bh - c * p.G);
-            const int k2 = rem / Gc;
-            bh = c * p.G + (rem - k2 * Gc);
-            kk = nh + k2;
-        }
+        const int nbh = (int)p.bh, C = (nbh + p.G - 1) / p.G;
+        int rem = item, kk = 0, bh = 0;
+        auto take = [&](int c, bool heavy) {
+            const int Gc = min(p.G, nbh - c * p.G), sz = (heavy ? nh : p.ntiles - nh) * Gc;
+            if (rem < sz) {
+                const int k2 = rem / Gc;
+                bh = c * p.G + (rem - k2 * Gc);
+                kk = heavy ? k2 : nh + k2;
+                return true;
+            }
+            rem -= sz;
+            return false;
+        };
+        bool found = false;
+        for (int c = 0; c < min(SPION_HEAVY_AHEAD, C) && !found; ++c) found = take(c, true);
+        for (int c = 0; c < C && !found; ++c)
+            found = (c + SPION_HEAVY_AHEAD < C && take(c + SPION_HEAVY_AHEAD, true)) || take(c, false);
         const int t = p.plan[p.off_order + kk];
         const int beg = p.plan[p.off_ptr + t], cnt = p.plan[p.off_ptr + t + 1] - beg;
         for (int e = lane; e < cnt; e += 32) {
