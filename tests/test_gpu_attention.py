@@ -213,3 +213,60 @@ def test_step_host_matches_device_calls():
     assert nnz.value == bp.nnzb
     for got, want in ((ho, o), (hlse, lse), (hdq, dq), (hdk, dk), (hdv, dv)):
         assert torch.equal(got, want.cpu())
+
+
+@pytest.mark.parametrize("L,B", [(1024, 32), (2048, 64), (4096, 64)])
+def test_plan_matches_host_recomputation(L, B):
+    """The attention work plan built by the pattern kernel (slot tiles of S = 128/B block rows /
+    columns, union lists with slot masks, descending-work order, heavy-tile counts) equals a
+    plain host recomputation from the block mask."""
+    spion = _spion()
+    A = synth.lra_scores(L, B, seed=3)
+    bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
+    n = L // B
+    fl = bp.mask.view(n, n).cpu().numpy().astype(bool)
+    plan = bp.plan.view(torch.int32).cpu().numpy()
+    S = 128 // B
+    nt = (n + S - 1) // S
+    fptr = 16
+    bptr = fptr + nt + 1
+    forder = bptr + nt + 1
+    border = forder + nt
+    cap = n * nt
+    fcol = border + nt
+    fmsk, brow = fcol + cap, fcol + 2 * cap
+    bmsk = brow + cap
+    assert list(plan[:3]) == [n, S, nt]
+    for which, (ptr, order, col, msk, grid) in enumerate(((fptr, forder, fcol, fmsk, fl), (bptr, border, brow, bmsk, fl.T))):
+        cnts = []
+        for t in range(nt):
+            rows = grid[t * S:(t + 1) * S]
+            union = np.nonzero(rows.any(0))[0]
+            beg, end = plan[ptr + t], plan[ptr + t + 1]
+            assert end - beg == len(union)
+            assert (plan[col + beg:col + end] == union).all()
+            want_m = [sum(int(rows[s, j]) << s for s in range(rows.shape[0])) for j in union]
+            assert list(plan[msk + beg:msk + end]) == want_m
+            cnts.append(len(union))
+        want_order = sorted(range(nt), key=lambda t: (-cnts[t], t))
+        assert list(plan[order:order + nt]) == want_order
+        tot = sum(cnts)
+        assert plan[5 + which] == sum(1 for c in cnts if c * nt > 2 * tot)
+
+
+def test_backward_deterministic():
+    """Every accumulator has one issuing thread and a fixed block order: two backward passes
+    give identical bits."""
+    spion = _spion()
+    L, B, bh, d = 2048, 64, 24, 64
+    A = synth.lra_scores(L, B, seed=9)
+    bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
+    q, k, v, do = (x.to(DEV) for x in synth.qkvdo(bh, L, d, seed=5, dtype=torch.bfloat16))
+    o, lse = spion.attn_fwd(q, k, v, bp)
+    g1 = spion.attn_bwd(q, k, v, o, do, lse, bp)
+    g1 = [x.clone() for x in g1]
+    o2, lse2 = spion.attn_fwd(q, k, v, bp)
+    g2 = spion.attn_bwd(q, k, v, o2, do, lse2, bp)
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
