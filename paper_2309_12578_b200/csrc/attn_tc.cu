@@ -184,18 +184,35 @@ struct Sched {
     int *hdr;  // [4][8]: item, bh, t, cnt, rc[0..3] (block-row counts of the slots)
     int *col;  // [4][SCHED_CAP]
     int *msk;  // [4][SCHED_CAP]
+    // copies of the plan's small arrays, loaded once per CTA (the per-item fetch then needs
+    // one global round trip for the tile's list, after the atomic): [0] heavy-tile count,
+    // order[ntiles] at TAB_ORDER, ptr[ntiles + 1] at TAB_PTR, block-row counts at TAB_RC
+    int *tab;
     uint64_t *full, *empty;  // [4] each
 };
-static constexpr int SCHED_BYTES = (32 + 2 * 4 * SCHED_CAP) * 4;
+static constexpr int TAB_ORDER = 8, TAB_PTR = TAB_ORDER + SCHED_CAP, TAB_RC = TAB_PTR + SCHED_CAP + 8;
+static constexpr int SCHED_TAB = TAB_RC + SCHED_CAP;
+static constexpr int SCHED_BYTES = (32 + 2 * 4 * SCHED_CAP + SCHED_TAB) * 4;
 
 __device__ __forceinline__ Sched make_sched(uint8_t *area, uint64_t *bars) {
     Sched s;
     s.hdr = reinterpret_cast<int *>(area);
     s.col = s.hdr + 32;
     s.msk = s.col + 4 * SCHED_CAP;
+    s.tab = s.msk + 4 * SCHED_CAP;
     s.full = bars;
     s.empty = bars + 4;
     return s;
+}
+
+// all threads, before the CTA's first __syncthreads: copy the plan's order, pointers and
+// (forward) block-row counts into shared memory
+__device__ __forceinline__ void sched_load_tables(const Sched &sc, const TcParams &p, bool want_rc) {
+    if (threadIdx.x == 0) sc.tab[0] = p.plan[p.off_heavy];
+    for (int i = threadIdx.x; i < p.ntiles; i += blockDim.x) sc.tab[TAB_ORDER + i] = p.plan[p.off_order + i];
+    for (int i = threadIdx.x; i <= p.ntiles; i += blockDim.x) sc.tab[TAB_PTR + i] = p.plan[p.off_ptr + i];
+    if (want_rc)
+        for (int i = threadIdx.x; i < p.n; i += blockDim.x) sc.tab[TAB_RC + i] = p.brow_ptr[i + 1] - p.brow_ptr[i];
 }
 
 // `consumers` warps release each slot: the MMA warp and every softmax warp
@@ -206,13 +223,20 @@ __device__ __forceinline__ void sched_init(const Sched &sc, int consumers = 5) {
     }
 }
 
-// whole producer warp; returns the item (-1 = no more work)
-__device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcParams &p, int nitems, bool want_rc) {
+// the next item's index from the plan's atomic counter (lane 0; the value is used by a later
+// sched_produce, so the atomic's round trip overlaps the current item's TMA issue)
+__device__ __forceinline__ int sched_prefetch(const TcParams &p) {
+    return (threadIdx.x & 31) == 0 ? atomicAdd(const_cast<int *>(p.plan) + p.off_sched, 1) : 0;
+}
+
+// whole producer warp; returns the item (-1 = no more work).  pre: a prefetched item index
+// (sched_prefetch, valid in lane 0), or -2 to fetch one now
+__device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcParams &p, int nitems, bool want_rc,
+                                             int pre = -2) {
     const int lane = threadIdx.x & 31;
     const int slot = k & 3;
     mbar_wait(sc.empty + slot, ((k >> 2) & 1) ^ 1);
-    int item = 0;
-    if (lane == 0) item = atomicAdd(const_cast<int *>(p.plan) + p.off_sched, 1);
+    int item = pre != -2 ? pre : sched_prefetch(p);
     item = __shfl_sync(0xffffffffu, item, 0);
     int *h = sc.hdr + slot * 8;
     if (item >= nitems) {
@@ -224,7 +248,7 @@ __device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcPar
         // before the light tiles of chunk c (A = SPION_HEAVY_AHEAD): long tiles start A chunks
         // early, so none is left for the end of the launch, while the L2 working set stays
         // A + 1 chunks.  Block order (A = 1): H0, H1, L0, H2, L1, ..., H(C-1), L(C-2), L(C-1)
-        const int nh = p.plan[p.off_heavy];
+        const int nh = sc.tab[0];
         const int nbh = (int)p.bh, C = (nbh + p.G - 1) / p.G;
         int rem = item, kk = 0, bh = 0;
         auto take = [&](int c, bool heavy) {
@@ -242,15 +266,15 @@ __device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcPar
         for (int c = 0; c < min(SPION_HEAVY_AHEAD, C) && !found; ++c) found = take(c, true);
         for (int c = 0; c < C && !found; ++c)
             found = (c + SPION_HEAVY_AHEAD < C && take(c + SPION_HEAVY_AHEAD, true)) || take(c, false);
-        const int t = p.plan[p.off_order + kk];
-        const int beg = p.plan[p.off_ptr + t], cnt = p.plan[p.off_ptr + t + 1] - beg;
+        const int t = sc.tab[TAB_ORDER + kk];
+        const int beg = sc.tab[TAB_PTR + t], cnt = sc.tab[TAB_PTR + t + 1] - beg;
         for (int e = lane; e < cnt; e += 32) {
             sc.col[slot * SCHED_CAP + e] = p.plan[p.off_col + beg + e];
             sc.msk[slot * SCHED_CAP + e] = p.plan[p.off_msk + beg + e];
         }
         if (want_rc && lane < 4) {
             const int I = t * p.S + lane;
-            h[4 + lane] = (lane < p.S && I < p.n) ? p.brow_ptr[I + 1] - p.brow_ptr[I] : 0;
+            h[4 + lane] = (lane < p.S && I < p.n) ? sc.tab[TAB_RC + I] : 0;
         }
         if (lane == 0) { h[0] = item; h[1] = bh; h[2] = t; h[3] = cnt; }
     }
@@ -365,6 +389,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::FWD_COLS>(tmem_slot);
+    sched_load_tables(sc, p, true);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -375,10 +400,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     if (warp == W_PROD) {
         // ------------------------------------------------------------ scheduler + TMA producer
         if (lane == 0) { prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmO); }
-        int st = 0, nq = 0;
+        int st = 0, nq = 0, pre = -2;  // pre: next item index, prefetched during this item
         uint32_t ph = 0;
         for (int ks = 0;; ++ks) {
-            const int item = sched_produce(sc, ks, p, nitems, true);
+            const int item = sched_produce(sc, ks, p, nitems, true, pre);
+            pre = -2;
             if (item < 0) break;
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], t = h[2], cnt = h[3];
@@ -393,6 +419,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 __syncwarp();
                 ++nq;
                 for (int j = 0; j < cnt; ++j) {
+                    if (j == (cnt > 2 ? cnt - 2 : 0)) pre = sched_prefetch(p);
                     mbar_wait(kv_empty + st, ph ^ 1);
                     if (elect_one()) {
                         if (SPION_DBG_NOLOAD) {
@@ -692,6 +719,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DQ_COLS>(tmem_slot);
+    sched_load_tables(sc, p, false);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -704,10 +732,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             prefetch_tmap(&tmQ); prefetch_tmap(&tmdO); prefetch_tmap(&tmO);
             prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmdQ);
         }
-        int st = 0, nq = 0;
+        int st = 0, nq = 0, pre = -2;  // pre: next item index, prefetched during this item
         uint32_t ph = 0;
         for (int ks = 0;; ++ks) {
-            const int item = sched_produce(sc, ks, p, nitems, false);
+            const int item = sched_produce(sc, ks, p, nitems, false, pre);
+            pre = -2;
             if (item < 0) break;
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], t = h[2], cnt = h[3];
@@ -729,6 +758,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 __syncwarp();
                 ++nq;
                 for (int j = 0; j < cnt; ++j) {
+                    if (j == (cnt > 2 ? cnt - 2 : 0)) pre = sched_prefetch(p);
                     mbar_wait(kv_empty + st, ph ^ 1);
                     if (elect_one()) {
                         if (SPION_DBG_NOLOAD) {
@@ -1016,6 +1046,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
+    sched_load_tables(sc, p, false);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1029,10 +1060,11 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmQ); prefetch_tmap(&tmdO);
             prefetch_tmap(&tmdK); prefetch_tmap(&tmdV);
         }
-        int st = 0, nk = 0;
+        int st = 0, nk = 0, pre = -2;  // pre: next item index, prefetched during this item
         uint32_t ph = 0;
         for (int ks = 0;; ++ks) {
-            const int item = sched_produce(sc, ks, p, nitems, false);
+            const int item = sched_produce(sc, ks, p, nitems, false, pre);
+            pre = -2;
             if (item < 0) break;
             if (lane == 0) tr.ev(1);
             const int *h = sc.hdr + (ks & 3) * 8;
@@ -1051,6 +1083,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 ++nk;
                 for (int j = 0; j < cnt; ++j) {
                     const int I = rows[j];
+                    if (j == (cnt > 2 ? cnt - 2 : 0)) pre = sched_prefetch(p);
                     mbar_wait(q_empty + st, ph ^ 1);
                     if (lane == 0) tr.ev(3);
                     uint8_t *stg = sStage + st * STAGE;
