@@ -58,6 +58,8 @@ def lib():
             "spion_oracle_flood_fill": (ctypes.c_int, [P, i32, P, P]),
             "spion_oracle_mask_to_bsr": (i64, [P, i32, P, P, P, P]),
             "spion_oracle_pattern": (ctypes.c_int, [P, i32, i32, i32, f64, i32, P, P, P]),
+            "spion_oracle_flood_fill_variant": (ctypes.c_int, [P, i32, P, i32, P]),
+            "spion_oracle_pattern_variant": (ctypes.c_int, [P, i32, i32, i32, f64, i32, i32, P, P, P]),
             "spion_oracle_attn_fwd": (ctypes.c_int, [P, P, P, i32, i32, i32, P, f64, i32, P, P, P]),
             "spion_oracle_attn_bwd": (ctypes.c_int, [P, P, P, P, i32, i32, i32, P, f64, i32, P, P, P]),
         }
@@ -120,12 +122,24 @@ def threshold_gt(pool: np.ndarray, B: int, theta: float, kind: str = "linear"):
     return gt, t.value
 
 
-def flood_fill(pool: np.ndarray, gt: np.ndarray) -> np.ndarray:
+# pattern variants: SPION-C, prose recursion (R2), all-cells seeding
+VARIANTS = {"noflood": 1, "prose": 2, "all_seeds": 4}
+
+
+def variant_bits(variant) -> int:
+    """'noflood' / 'prose' / 'all_seeds' (or a '+'-joined combination, or an int) -> flag bits."""
+    if isinstance(variant, int):
+        return variant
+    return sum(VARIANTS[v] for v in variant.split("+")) if variant else 0
+
+
+def flood_fill(pool: np.ndarray, gt: np.ndarray, variant=0) -> np.ndarray:
     pool = np.ascontiguousarray(pool, dtype=np.int64)
     gt = np.ascontiguousarray(gt, dtype=np.uint8)
     n = pool.shape[0]
     fl = np.empty((n, n), dtype=np.uint8)
-    _check(lib().spion_oracle_flood_fill(_ptr(pool), n, _ptr(gt), _ptr(fl)), "flood_fill")
+    _check(lib().spion_oracle_flood_fill_variant(_ptr(pool), n, _ptr(gt), variant_bits(variant), _ptr(fl)),
+           "flood_fill")
     return fl
 
 
@@ -148,8 +162,8 @@ def mask_to_bsr(fl: np.ndarray):
     }
 
 
-def pattern(A: np.ndarray, B: int, F: int = 31, theta: float = 96.0, kind: str = "linear"):
-    """Alg. 3 end to end. Returns (fl_out uint8 [n][n], pool int64 [n][n], t)."""
+def pattern(A: np.ndarray, B: int, F: int = 31, theta: float = 96.0, kind: str = "linear", variant=0):
+    """Alg. 3 end to end (variant: see VARIANTS). Returns (fl_out uint8 [n][n], pool int64 [n][n], t)."""
     A = np.ascontiguousarray(A, dtype=np.float32)
     L = A.shape[0]
     if A.shape != (L, L) or B <= 0 or L % B:
@@ -159,8 +173,8 @@ def pattern(A: np.ndarray, B: int, F: int = 31, theta: float = 96.0, kind: str =
     fl = np.empty((n, n), np.uint8)
     t = ctypes.c_double(0.0)
     _check(
-        lib().spion_oracle_pattern(_ptr(A), L, B, F, float(theta), _KINDS[kind], _ptr(pool), _ptr(fl),
-                                   ctypes.byref(t)),
+        lib().spion_oracle_pattern_variant(_ptr(A), L, B, F, float(theta), _KINDS[kind], variant_bits(variant),
+                                           _ptr(pool), _ptr(fl), ctypes.byref(t)),
         "pattern",
     )
     return fl, pool, t.value

@@ -24,6 +24,10 @@
  *   spion_oracle_threshold_gt   pinned (numpy.quantile, nearest-rank examples)
  *   spion_oracle_flood_fill     pinned (SPEC worked examples; exhaustive
  *                               literal-recursion Alg. 4 on 3x3 grids)
+ *   ..._flood_fill_variant      pinned (SPION-C = definition; prose recursion
+ *                               and all-cells seeding against unpruned
+ *                               recursions written in the test, exhaustive
+ *                               3x3 grids; all-seeds closed form; R2 within R1)
  *   spion_oracle_pattern        pinned (composition + invariants P7)
  *   spion_oracle_mask_to_bsr    pinned (S:125 worked example, invariants)
  *   spion_oracle_attn_fwd/bwd   pinned (SDPA fp64 on all-ones and boolean
@@ -211,20 +215,78 @@ static void flood_fill(const int64_t *pool_out, int32_t n, int32_t r, int32_t c,
     }
 }
 
+/* The prose reading of the recursion (reading Q11 R2): "after
+ * determining the critical element, the algorithm recursively compares the
+ * elements to the right, below and diagonally below the critical element" —
+ * recursion continues only from a neighbour that is marked (> t).  Each cell
+ * is marked (and entered) at most once, so no pruning is needed. */
+static void flood_fill_prose(const int64_t *pool_out, int32_t n, int32_t r, int32_t c, uint8_t *fl_out,
+                             const uint8_t *gt)
+{
+    /* Alg. 4 l.1-2: stop at the last row / column */
+    if (r + 1 == n || c + 1 == n) return;
+    int64_t below = pool_out[(int64_t)(r + 1) * n + c];
+    int64_t right = pool_out[(int64_t)r * n + (c + 1)];
+    int64_t diag = pool_out[(int64_t)(r + 1) * n + (c + 1)];
+    /* Alg. 4 l.3 */
+    int64_t m = below;
+    if (right > m) m = right;
+    if (diag > m) m = diag;
+    /* below, right, diagonally below: a max neighbour above t becomes critical and is recursed from */
+    int64_t k = (int64_t)(r + 1) * n + c;
+    if (below == m && fl_out[k] == 0 && gt[k]) { fl_out[k] = 1; flood_fill_prose(pool_out, n, r + 1, c, fl_out, gt); }
+    k = (int64_t)r * n + (c + 1);
+    if (right == m && fl_out[k] == 0 && gt[k]) { fl_out[k] = 1; flood_fill_prose(pool_out, n, r, c + 1, fl_out, gt); }
+    k = (int64_t)(r + 1) * n + (c + 1);
+    if (diag == m && fl_out[k] == 0 && gt[k]) { fl_out[k] = 1; flood_fill_prose(pool_out, n, r + 1, c + 1, fl_out, gt); }
+}
+
+/* Pattern variants (flag bits shared in meaning, not in
+ * code, with the product's spion_pattern_variant):
+ *   ORACLE_PAT_NOFLOOD   1: SPION-C: no flood fill, the top alpha%
+ *                           of pool_out (the gt cells) plus the forced diagonal
+ *                           (reading Q23)
+ *   ORACLE_PAT_PROSE     2: recursion only from critical (> t) cells (R2)
+ *   ORACLE_PAT_ALL_SEEDS 4: every element of pool_out a seed point */
+#define ORACLE_PAT_NOFLOOD 1
+#define ORACLE_PAT_PROSE 2
+#define ORACLE_PAT_ALL_SEEDS 4
+
 /* Alg. 3 lines 4-10: seeds (0,i) for all i, then (j,0) for
- * all j (reading Q12), then the forced diagonal.  Seeds are not
- * marked themselves (reading Q21).  fl_out must hold n*n bytes. */
-int spion_oracle_flood_fill(const int64_t *pool_out, int32_t n, const uint8_t *gt, uint8_t *fl_out)
+ * all j (reading Q12) — or every cell (ORACLE_PAT_ALL_SEEDS) — then the
+ * forced diagonal.  Seeds are not marked themselves (reading Q21).
+ * fl_out must hold n*n bytes. */
+int spion_oracle_flood_fill_variant(const int64_t *pool_out, int32_t n, const uint8_t *gt, int32_t variant,
+                                    uint8_t *fl_out)
 {
     if (n <= 0) return SPION_ORACLE_ERR_SHAPE;
-    uint8_t *explored = (uint8_t *)calloc((size_t)n * n, 1);
-    if (!explored) return SPION_ORACLE_ERR_PARAM;
+    if (variant & ~7) return SPION_ORACLE_ERR_PARAM;
     memset(fl_out, 0, (size_t)n * n);
-    for (int32_t i = 0; i < n; ++i) flood_fill(pool_out, n, 0, i, fl_out, gt, explored);
-    for (int32_t j = 0; j < n; ++j) flood_fill(pool_out, n, j, 0, fl_out, gt, explored);
+    if (variant & ORACLE_PAT_NOFLOOD) {
+        for (int64_t k = 0; k < (int64_t)n * n; ++k) fl_out[k] = gt[k] ? 1 : 0;
+    } else if (variant & ORACLE_PAT_PROSE) {
+        for (int32_t r = 0; r < n; ++r)
+            for (int32_t c = 0; c < n; ++c)
+                if ((variant & ORACLE_PAT_ALL_SEEDS) || r == 0 || c == 0) flood_fill_prose(pool_out, n, r, c, fl_out, gt);
+    } else {
+        uint8_t *explored = (uint8_t *)calloc((size_t)n * n, 1);
+        if (!explored) return SPION_ORACLE_ERR_PARAM;
+        if (variant & ORACLE_PAT_ALL_SEEDS) {
+            for (int32_t r = 0; r < n; ++r)
+                for (int32_t c = 0; c < n; ++c) flood_fill(pool_out, n, r, c, fl_out, gt, explored);
+        } else {
+            for (int32_t i = 0; i < n; ++i) flood_fill(pool_out, n, 0, i, fl_out, gt, explored);
+            for (int32_t j = 0; j < n; ++j) flood_fill(pool_out, n, j, 0, fl_out, gt, explored);
+        }
+        free(explored);
+    }
     for (int32_t k = 0; k < n; ++k) fl_out[(int64_t)k * n + k] = 1;
-    free(explored);
     return SPION_ORACLE_OK;
+}
+
+int spion_oracle_flood_fill(const int64_t *pool_out, int32_t n, const uint8_t *gt, uint8_t *fl_out)
+{
+    return spion_oracle_flood_fill_variant(pool_out, n, gt, 0, fl_out);
 }
 
 /* ------------------------------------------------------------------ */
@@ -257,8 +319,8 @@ int64_t spion_oracle_mask_to_bsr(const uint8_t *fl, int32_t n, int32_t *brow_ptr
 /* flood fill, forced diagonal.  pool_out (n*n) and fl_out (n*n) are    */
 /* outputs; t_out receives the threshold in pool-sum units.             */
 /* ------------------------------------------------------------------ */
-int spion_oracle_pattern(const float *A, int32_t L, int32_t B, int32_t F, double theta, int32_t kind,
-                         int64_t *pool_out, uint8_t *fl_out, double *t_out)
+int spion_oracle_pattern_variant(const float *A, int32_t L, int32_t B, int32_t F, double theta, int32_t kind,
+                                 int32_t variant, int64_t *pool_out, uint8_t *fl_out, double *t_out)
 {
     if (L <= 0 || B <= 0 || (L % B) != 0) return SPION_ORACLE_ERR_SHAPE;
     if (F < 1 || (F % 2) == 0) return SPION_ORACLE_ERR_PARAM;
@@ -277,12 +339,18 @@ int spion_oracle_pattern(const float *A, int32_t L, int32_t B, int32_t F, double
     if (rc) goto done;
     rc = spion_oracle_threshold_gt(pool_out, (int64_t)n * n, B, theta, kind, gt, t_out); /* P:600 */
     if (rc) goto done;
-    rc = spion_oracle_flood_fill(pool_out, n, gt, fl_out);  /* Alg. 3 l.4-10 */
+    rc = spion_oracle_flood_fill_variant(pool_out, n, gt, variant, fl_out);  /* Alg. 3 l.4-10 */
 done:
     free(q);
     free(conv);
     free(gt);
     return rc;
+}
+
+int spion_oracle_pattern(const float *A, int32_t L, int32_t B, int32_t F, double theta, int32_t kind,
+                         int64_t *pool_out, uint8_t *fl_out, double *t_out)
+{
+    return spion_oracle_pattern_variant(A, L, B, F, theta, kind, 0, pool_out, fl_out, t_out);
 }
 
 /* ------------------------------------------------------------------ */

@@ -321,3 +321,98 @@ def test_pattern_rejects_bad_params():
     A[0, 0] = 2.0
     with pytest.raises(oracle.OracleError):
         oracle.pattern(A, 4, 3, 90.0)   # score outside [0,1]
+
+
+# ------------------------------------------------------ NEXT-2 pattern variants
+def _literal_variant(pool, t, prose=False, all_seeds=False, order=(0, 1, 2)):
+    """Alg. 4 written out again with the two readings of SURVEY Q11/Q12, no pruning:
+    prose (R2): the recursion continues only from a critical (> t) neighbour (P:602-603);
+    all_seeds: every element of pool_out is a seed point."""
+    n = len(pool)
+    fl = [[0] * n for _ in range(n)]
+
+    def ff(r, c):
+        if r + 1 == n or c + 1 == n:
+            return
+        nb = [(r + 1, c), (r, c + 1), (r + 1, c + 1)]
+        m = max(pool[a][b] for a, b in nb)
+        for k in order:
+            a, b = nb[k]
+            if pool[a][b] == m and fl[a][b] == 0:
+                if pool[a][b] > t:
+                    fl[a][b] = 1
+                    ff(a, b)
+                elif not prose:
+                    ff(a, b)
+
+    seeds = [(r, c) for r in range(n) for c in range(n)] if all_seeds else \
+        [(0, i) for i in range(n)] + [(j, 0) for j in range(n)]
+    for r, c in seeds:
+        ff(r, c)
+    for k in range(n):
+        fl[k][k] = 1
+    return np.array(fl, np.uint8)
+
+
+def _var(pool, t, variant):
+    pool = np.array(pool, np.int64)
+    return oracle.flood_fill(pool, (pool > t).astype(np.uint8), variant)
+
+
+def test_spion_c_is_threshold_plus_diagonal():
+    """SPION-C (P:825-826): the top alpha% of pool_out, no flood fill (+ forced diagonal, Q23);
+    end to end equals x > numpy.quantile(pool, alpha/100) on the oracle's own pool sums."""
+    rng = np.random.default_rng(4)
+    A = syn_scores(256, 16, heads=2, seed=8).numpy()
+    for alpha in (50.0, 75.0, 96.0):
+        fl, pool, _ = oracle.pattern(A, 16, 31, alpha, variant="noflood")
+        want = (pool > np.quantile(pool.astype(np.float64), alpha / 100.0)) | np.eye(pool.shape[0], dtype=bool)
+        assert (fl.astype(bool) == want).all()
+    pool = rng.integers(0, 9, size=(7, 7))
+    assert (_var(pool, 4, "noflood").astype(bool) == ((pool > 4) | np.eye(7, dtype=bool))).all()
+
+
+def test_variants_exhaustive_3x3_literal_recursion():
+    """All 3^9 grids over {1,5,9} x t in {1,5}: prose recursion, all-cells seeding and both
+    together == the unpruned literal recursions above (two visit orders)."""
+    vals = (1, 5, 9)
+    for cells in itertools.product(vals, repeat=9):
+        pool = [list(cells[0:3]), list(cells[3:6]), list(cells[6:9])]
+        for t in (1, 5):
+            for prose, seeds, v in ((True, False, "prose"), (False, True, "all_seeds"), (True, True, "prose+all_seeds")):
+                want = _literal_variant(pool, t, prose, seeds)
+                assert (want == _literal_variant(pool, t, prose, seeds, order=(2, 1, 0))).all()
+                assert (_var(pool, t, v) == want).all(), (pool, t, v)
+
+
+@pytest.mark.parametrize("n", [5, 8, 16])
+def test_variant_invariants_random(n):
+    """R2 marks a subset of Alg. 4; all-cells seeding a superset; with every
+    cell a seed, R1 and R2 coincide and equal the closed form: cells entered by a
+    max-neighbour edge from any cell, above t, plus the diagonal."""
+    rng = np.random.default_rng(n)
+    for trial in range(40):
+        pool = rng.integers(0, 5, size=(n, n))
+        t = int(rng.integers(0, 5))
+        base, prose, alls = _var(pool, t, 0), _var(pool, t, "prose"), _var(pool, t, "all_seeds")
+        assert (prose <= base).all() and (base <= alls).all()
+        assert (alls == _var(pool, t, "prose+all_seeds")).all()
+        entered = np.zeros((n, n), bool)
+        for r in range(n - 1):
+            for c in range(n - 1):
+                nb = [(r + 1, c), (r, c + 1), (r + 1, c + 1)]
+                m = max(pool[a, b] for a, b in nb)
+                for a, b in nb:
+                    entered[a, b] |= pool[a, b] == m
+        want = (entered & (pool > t)) | np.eye(n, dtype=bool)
+        assert (alls.astype(bool) == want).all()
+        if n <= 8:
+            assert (prose == _literal_variant(pool.tolist(), t, prose=True)).all()
+
+
+def test_variants_worked_example(golden_dir):
+    """Hand-worked example separating the literal recursion from the prose reading."""
+    g = _load(golden_dir, "flood_fill_variants.json")
+    for case in g["cases"]:
+        for v, want in case["fl"].items():
+            assert (_var(case["pool"], case["t"], v) == np.array(want, np.uint8)).all(), v
