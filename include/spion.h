@@ -75,6 +75,22 @@ typedef enum {
     SPION_TH_ABSOLUTE = 2
 } spion_threshold_kind;
 
+/* Pattern variants, bit flags for spion_pattern_variant:
+ *   SPION_PAT_NOFLOOD   SPION-C: no flood fill; the top alpha% of
+ *                       pool_out (the cells > t) plus the forced diagonal
+ *                       (reading Q23).  SPION-F (no convolution) is filter = 1.
+ *   SPION_PAT_PROSE     the prose reading of Alg. 4 (reading Q11 R2):
+ *                       the fill continues only from critical (> t) cells.
+ *   SPION_PAT_ALL_SEEDS every element of pool_out is a seed point (
+ *                       reading Q12), instead of row 0 and column 0 (Alg. 3).
+ * 0 is Alg. 3/4 as printed (SPION-CF, the paper's model). */
+typedef enum {
+    SPION_PAT_DEFAULT = 0,
+    SPION_PAT_NOFLOOD = 1,
+    SPION_PAT_PROSE = 2,
+    SPION_PAT_ALL_SEEDS = 4
+} spion_pattern_flags;
+
 /* Block pattern in block-CSR + block-CSC form (CSR of P; the nearest
  * neighbour upsampling of Alg. 3 l.11 is implicit: block
  * (I,J) stands for the B x B all-ones square of P).  All pointers are
@@ -122,6 +138,13 @@ SPION_API size_t spion_pattern_workspace_bytes(int32_t L, int32_t block);
 SPION_API spion_status spion_pattern(const float *scores_dev, int32_t L, int32_t block, int32_t filter,
                            double threshold, spion_threshold_kind kind, void *ws_dev, size_t ws_bytes,
                            spion_bsr *out, int32_t *nnzb_host, void *stream);
+
+/* spion_pattern with a variant: `variant` is a bitwise OR of spion_pattern_flags
+ * (any combination; NOFLOOD ignores the other two).  Other bits: SPION_ERR_PARAM.
+ * Results are bit-identical to the oracle's spion_oracle_pattern_variant. */
+SPION_API spion_status spion_pattern_variant(const float *scores_dev, int32_t L, int32_t block, int32_t filter,
+                           double threshold, spion_threshold_kind kind, uint32_t variant, void *ws_dev,
+                           size_t ws_bytes, spion_bsr *out, int32_t *nnzb_host, void *stream);
 
 /* Synchronises `stream` and reads the device flag word of a pattern
  * workspace: *flags_host = 0 if every score was finite and in [0,1]. */

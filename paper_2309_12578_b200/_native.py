@@ -13,6 +13,8 @@ STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace"
 F32, BF16 = 0, 1
 SOFTMAX = {"paper": 0, "masked": 1}
 THRESH = {"linear": 0, "nearest": 1, "absolute": 2}
+# spion_pattern_flags (include/spion.h): SPION-C, prose recursion, all-cells seeding
+PATTERN_VARIANTS = {"noflood": 1, "prose": 2, "all_seeds": 4}
 
 
 class SpionError(RuntimeError):
@@ -36,6 +38,9 @@ EXPORTS = {
     "spion_pattern": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(BSR),
                                      ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_pattern_variant": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_double, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p,
+                                             ctypes.c_size_t, ctypes.POINTER(BSR), ctypes.c_void_p, ctypes.c_void_p]),
     "spion_pattern_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "spion_bsr_from_mask": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BSR),
                                            ctypes.c_void_p, ctypes.c_void_p]),

@@ -80,7 +80,15 @@ static spion_status check_bsr_out(const spion_bsr *out, int32_t L, int32_t block
 spion_status spion_pattern(const float *scores_dev, int32_t L, int32_t block, int32_t filter, double threshold,
                            spion_threshold_kind kind, void *ws_dev, size_t ws_bytes, spion_bsr *out,
                            int32_t *nnzb_host, void *stream) {
+    return spion_pattern_variant(scores_dev, L, block, filter, threshold, kind, SPION_PAT_DEFAULT, ws_dev, ws_bytes,
+                                 out, nnzb_host, stream);
+}
+
+spion_status spion_pattern_variant(const float *scores_dev, int32_t L, int32_t block, int32_t filter,
+                                   double threshold, spion_threshold_kind kind, uint32_t variant, void *ws_dev,
+                                   size_t ws_bytes, spion_bsr *out, int32_t *nnzb_host, void *stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (variant & ~7u) return SPION_ERR_PARAM;
     if (L <= 0 || block <= 0 || L % block) return SPION_ERR_SHAPE;
     if (filter < 1 || filter % 2 == 0) return SPION_ERR_PARAM;
     if (!scores_dev || !ws_dev) return SPION_ERR_PARAM;
@@ -127,7 +135,7 @@ spion_status spion_pattern(const float *scores_dev, int32_t L, int32_t block, in
         }
         default: return SPION_ERR_PARAM;
     }
-    st = launch_pattern(scores_dev, L, block, filter, (int)kind, lo, frac_pos, T_abs, ws_dev, out, s);
+    st = launch_pattern(scores_dev, L, block, filter, (int)kind, lo, frac_pos, (int)variant, T_abs, ws_dev, out, s);
     if (st) return st;
     if (nnzb_host) {
         int flags = 0;

@@ -332,6 +332,7 @@ struct K2Args {
     long long lo;           // LINEAR: floor(hpos); NEAREST: rank k
     int frac_pos;           // LINEAR: frac > 0
     long long T_abs;        // ABSOLUTE: gt <=> x > T_abs
+    int variant;            // spion_pattern_flags
     int *flags;
     int *brow_ptr, *bcol_idx, *bcol_ptr, *brow_idx, *nnzb;
     uint8_t *mask;
@@ -595,7 +596,44 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
     //   That recurrence is a carry chain: with g = X & rt, p = rt the carries of g + p are
     //   C[c] = R[c-1] & rt[c-1] (the cells entered by a right edge); R = X | C.
     //   marked = (entered by an edge AND > t) (Alg. 4 l.5-7) OR diagonal (Alg. 3 l.9-10)
-    if (tid == 0 && n <= 64) {  // the same sweep on 64-bit rows (half the dependent ops)
+    if (a.variant & (SPION_PAT_NOFLOOD | SPION_PAT_ALL_SEEDS)) {
+        // no sweep needed.  SPION-C: marked = gt.  Every cell a seed: every cell propagates (so the
+        // literal and prose readings coincide), marked = entered by an edge from any cell AND gt,
+        // where row r is entered from row r-1 (down / diagonal edges) or from its left neighbour
+        const bool nof = a.variant & SPION_PAT_NOFLOOD;
+        for (int r = tid; r < n; r += blockDim.x) {
+            const Bits gt = b_load(gtw + r * 4);
+            Bits fl = gt;
+            if (!nof) {
+                Bits E = b_shl1(b_load(rtw + r * 4));
+                if (r > 0) E = b_or(E, b_or(b_load(dnw + (r - 1) * 4), b_shl1(b_load(dgw + (r - 1) * 4))));
+                fl = b_and(E, gt);
+            }
+            b_store(sc.flw + r * 4, b_and(b_or(fl, b_bit(r)), b_ones(n)));
+        }
+    } else if (a.variant & SPION_PAT_PROSE) {
+        // prose reading: only the seeds and the marked cells propagate.  Along row r the edge
+        // c -> c+1 is usable when rt[c] and gt[c+1] (the cell it enters becomes critical), so the
+        // propagating set is the same carry chain as below with rt replaced by that link mask
+        if (tid == 0) {
+            const Bits all = b_ones(n);
+            Bits prop{0ull, 0ull}, dn{0ull, 0ull}, dg{0ull, 0ull};
+            for (int r = 0; r < n; ++r) {
+                const Bits rt = b_load(rtw + r * 4), gt = b_load(gtw + r * 4);
+                const Bits E = b_or(b_and(prop, dn), b_shl1(b_and(prop, dg)));  // entered from above
+                const Bits seed = r == 0 ? all : Bits{1ull, 0ull};
+                const Bits X = b_or(seed, b_and(E, gt));
+                const Bits lnk = b_and(rt, Bits{(gt.lo >> 1) | (gt.hi << 63), gt.hi >> 1});
+                const Bits gg = b_and(X, lnk);
+                const Bits C = b_xor(b_add(gg, lnk), b_xor(gg, lnk));  // entered from the left, critical
+                prop = b_or(X, C);
+                const Bits entered = b_or(E, b_shl1(b_and(prop, rt)));
+                b_store(sc.flw + r * 4, b_and(b_or(b_and(entered, gt), b_bit(r)), all));
+                dn = b_load(dnw + r * 4);
+                dg = b_load(dgw + r * 4);
+            }
+        }
+    } else if (tid == 0 && n <= 64) {  // the same sweep on 64-bit rows (half the dependent ops)
         const unsigned long long all = ~0ull >> (64 - n);
         unsigned long long vis = 0ull, dn = 0ull, dg = 0ull;
 #pragma unroll 4
@@ -675,7 +713,7 @@ static size_t k2_smem_bytes(int n, bool with_pool) {
     return b;
 }
 
-spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos,
+spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos, int variant,
                             long long T_abs, void *ws, spion_bsr *out, cudaStream_t s) {
     const int n = L / B;
     if (n > K2_MAXN) return SPION_ERR_UNSUPPORTED;
@@ -701,6 +739,7 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     a.lo = lo;
     a.frac_pos = frac_pos;
     a.T_abs = T_abs;
+    a.variant = variant;
     a.flags = flags;
     a.brow_ptr = out->brow_ptr;
     a.bcol_idx = out->bcol_idx;

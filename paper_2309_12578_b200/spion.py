@@ -97,11 +97,12 @@ def empty_pattern(L: int, block: int, device) -> BlockPattern:
 
 def pattern(scores: torch.Tensor, block: int, filter: int = 31, alpha: Optional[float] = None,
             t: Optional[float] = None, kind: str = "linear", out: Optional[BlockPattern] = None,
-            sync: bool = False) -> BlockPattern:
+            sync: bool = False, variant: str = "") -> BlockPattern:
     """Alg. 3: scores [L][L] fp32 in [0,1] -> block pattern.
 
     Give ``alpha`` (percent, quantile threshold, ``kind`` linear|nearest) or ``t``
-    (absolute threshold in pool-mean units)."""
+    (absolute threshold in pool-mean units).  ``variant``: "" (Alg. 3/4, SPION-CF) or a
+    '+'-joined subset of noflood (SPION-C), prose (reading R2), all_seeds; SPION-F is filter=1."""
     _require_cuda(scores)
     if scores.dtype != torch.float32 or scores.dim() != 2 or scores.shape[0] != scores.shape[1]:
         raise ValueError("scores must be a square fp32 matrix")
@@ -120,8 +121,10 @@ def pattern(scores: torch.Tensor, block: int, filter: int = 31, alpha: Optional[
         bp.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=scores.device)
     s = bp.c_struct()
     nnz = ctypes.c_int32(0)
-    st = lib.spion_pattern(_p(scores), L, block, filter, theta, N.THRESH[kind], _p(bp.workspace), ws_bytes,
-                           ctypes.byref(s), ctypes.byref(nnz) if sync else None, _stream(scores.device))
+    bits = sum(N.PATTERN_VARIANTS[v] for v in variant.split("+")) if variant else 0
+    st = lib.spion_pattern_variant(_p(scores), L, block, filter, theta, N.THRESH[kind], bits, _p(bp.workspace),
+                                   ws_bytes, ctypes.byref(s), ctypes.byref(nnz) if sync else None,
+                                   _stream(scores.device))
     N.check(st, "spion_pattern")
     return bp
 

@@ -110,3 +110,33 @@ def test_bsr_from_mask_rejects_non_binary():
     with pytest.raises(N.SpionError) as e:
         spion.bsr_from_mask(torch.from_numpy(m).to(DEV), 256, 32)
     assert e.value.status == 3
+
+
+VARIANTS = ["noflood", "prose", "all_seeds", "prose+all_seeds"]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("L,B,F,theta", [(64, 8, 31, 75.0), (1024, 32, 31, 96.0), (1024, 32, 31, 60.0),
+                                         (2048, 64, 31, 75.0), (4096, 64, 31, 99.0), (4096, 32, 31, 90.0),
+                                         (192, 64, 31, 50.0), (96, 4, 63, 60.0)])
+def test_pattern_variants_bit_exact(variant, L, B, F, theta):
+    """NEXT-2 variants (SPION-C, prose recursion, all-cells seeding) bit-exact against the oracle,
+    including the 64-/128-bit row paths (n <= 64 / n = 128)."""
+    spion = _spion()
+    A = synth.lra_scores(L, B, seed=L + F) if L >= 1024 else synth.syn_scores(L, B, heads=2, seed=L + F)
+    bp = spion.pattern(A.to(DEV), B, filter=F, alpha=theta, sync=True, variant=variant)
+    fl_ref, _, _ = oracle.pattern(A.numpy(), B, F, theta, "linear", variant=variant)
+    _check(bp, fl_ref)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_pattern_variants_ties(seed, variant):
+    spion = _spion()
+    rng = np.random.default_rng(100 + seed)
+    L, B = 256, 16
+    A = (rng.integers(0, 4, size=(L, L)) / 3.0).astype(np.float32)
+    for alpha in (10.0, 50.0, 90.0):
+        bp = spion.pattern(torch.from_numpy(A).to(DEV), B, filter=7, alpha=alpha, sync=True, variant=variant)
+        fl_ref, _, _ = oracle.pattern(A, B, 7, alpha, variant=variant)
+        _check(bp, fl_ref)
