@@ -59,6 +59,8 @@ def lib():
             "spion_oracle_mask_to_bsr": (i64, [P, i32, P, P, P, P]),
             "spion_oracle_pattern": (ctypes.c_int, [P, i32, i32, i32, f64, i32, P, P, P]),
             "spion_oracle_flood_fill_variant": (ctypes.c_int, [P, i32, P, i32, P]),
+            "spion_oracle_score_mean": (ctypes.c_int, [P, P, i64, i32, i32, f64, P, P]),
+            "spion_oracle_transition": (ctypes.c_int, [f64, f64, f64, f64, P, P]),
             "spion_oracle_pattern_variant": (ctypes.c_int, [P, i32, i32, i32, f64, i32, i32, P, P, P]),
             "spion_oracle_attn_fwd": (ctypes.c_int, [P, P, P, i32, i32, i32, P, f64, i32, P, P, P]),
             "spion_oracle_attn_bwd": (ctypes.c_int, [P, P, P, P, i32, i32, i32, P, f64, i32, P, P, P]),
@@ -216,3 +218,26 @@ def attn_bwd(Q, K, V, dO, fl, B: int, scale: float, mode: str = "paper"):
         "attn_bwd",
     )
     return dQ, dK, dV
+
+
+# -------------------------------------------------------------- NEXT-1: dense-phase scores
+def score_mean(Q, K, scale: float):
+    """A^s = mean over (batch, head) of softmax(scale Q K^T), fp64; Q, K [bh][L][d].
+    Returns (A [L][L], sum of A^2)."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    K = np.ascontiguousarray(K, dtype=np.float64)
+    bh, L, d = Q.shape
+    A = np.empty((L, L), np.float64)
+    ss = ctypes.c_double(0.0)
+    _check(lib().spion_oracle_score_mean(_ptr(Q), _ptr(K), bh, L, d, float(scale), _ptr(A), ctypes.byref(ss)),
+           "score_mean")
+    return A, ss.value
+
+
+def transition(sumsq_im2: float, sumsq_im1: float, sumsq_i: float, alpha: float):
+    """Alg. 2 / Eq. 2 transition test from three consecutive sums of squares -> (bool, d_{i-1}, d_i)."""
+    d1, d2 = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    r = lib().spion_oracle_transition(float(sumsq_im2), float(sumsq_im1), float(sumsq_i), float(alpha),
+                                      ctypes.byref(d1), ctypes.byref(d2))
+    return bool(r), d1.value, d2.value
+

@@ -30,6 +30,8 @@
  *                               3x3 grids; all-seeds closed form; R2 within R1)
  *   spion_oracle_pattern        pinned (composition + invariants P7)
  *   spion_oracle_mask_to_bsr    pinned (S:125 worked example, invariants)
+ *   spion_oracle_score_mean     pinned (torch softmax fp64, rows sum to 1, Frobenius
+ *                               norm via numpy); _transition: Eq. 2 worked numbers
  *   spion_oracle_attn_fwd/bwd   pinned (SDPA fp64 on all-ones and boolean
  *                               masks, PAPER/MASKED closed form
  *                               worked example, finite differences)
@@ -456,3 +458,56 @@ int spion_oracle_attn_bwd(const double *Q, const double *K, const double *V, con
     free(lse);
     return SPION_ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* the dense-phase score matrix that feeds a1.    */
+/* A^s = mean over the `bh` (batch, head) slices of the dense attention */
+/* probabilities softmax(scale * Q K^T) (the "attention score matrix"   */
+/* averaged across heads; batch mean: SURVEY §8(a) a1), written  */
+/* as the definition: every row an explicit max / exp / sum in fp64.    */
+/* Q, K: [bh][L][d] fp64 (bf16 inputs widened exactly).  A: [L][L].    */
+/* sumsq (may be NULL): sum of A^2, the square of Eq. 2's norm. */
+/* ------------------------------------------------------------------ */
+int spion_oracle_score_mean(const double *Q, const double *K, int64_t bh, int32_t L, int32_t d, double scale,
+                            double *A, double *sumsq)
+{
+    if (bh <= 0 || L <= 0 || d <= 0) return SPION_ORACLE_ERR_SHAPE;
+    double *s = (double *)malloc(sizeof(double) * (size_t)L);
+    if (!s) return SPION_ORACLE_ERR_PARAM;
+    memset(A, 0, sizeof(double) * (size_t)L * L);
+    for (int64_t b = 0; b < bh; ++b) {
+        const double *q = Q + b * L * d, *k = K + b * L * d;
+        for (int32_t i = 0; i < L; ++i) {
+            double m = -INFINITY, Z = 0.0;
+            for (int32_t j = 0; j < L; ++j) {
+                double dot = 0.0;
+                for (int32_t e = 0; e < d; ++e) dot += q[(int64_t)i * d + e] * k[(int64_t)j * d + e];
+                s[j] = dot * scale;
+                if (s[j] > m) m = s[j];
+            }
+            for (int32_t j = 0; j < L; ++j) Z += exp(s[j] - m);
+            for (int32_t j = 0; j < L; ++j) A[(int64_t)i * L + j] += exp(s[j] - m) / Z / (double)bh;
+        }
+    }
+    if (sumsq) {
+        double acc = 0.0;
+        for (int64_t k2 = 0; k2 < (int64_t)L * L; ++k2) acc += A[k2] * A[k2];
+        *sumsq = acc;
+    }
+    free(s);
+    return SPION_ORACLE_OK;
+}
+
+/* Eq. 2: distance_i = | sqrt(sum (A^s_{i-1})^2) - sqrt(sum (A^s_i)^2) |, and Alg. 2's
+ * transition test: with three consecutive score matrices (i > 1),
+ * transition <=> sqrt((distance_{i-1} - distance_i)^2) < alpha.  Inputs: the three sums of squares. */
+int spion_oracle_transition(double sumsq_im2, double sumsq_im1, double sumsq_i, double alpha, double *dist_im1,
+                            double *dist_i)
+{
+    double d1 = fabs(sqrt(sumsq_im2) - sqrt(sumsq_im1));
+    double d2 = fabs(sqrt(sumsq_im1) - sqrt(sumsq_i));
+    if (dist_im1) *dist_im1 = d1;
+    if (dist_i) *dist_i = d2;
+    return sqrt((d1 - d2) * (d1 - d2)) < alpha ? 1 : 0;
+}
+

@@ -166,3 +166,26 @@ def test_p14_locality_block_diagonal():
     O2, _ = oracle.attn_fwd(Q, K, V2, fl, B, 0.4, "paper")
     assert (O1[:8] == O2[:8]).all()
     assert not (O1[8:16] == O2[8:16]).all()
+
+
+# ------------------------------------------------------ NEXT-1: dense-phase score capture
+def test_score_mean_matches_torch_softmax():
+    """A^s = mean over (batch, head) of softmax(scale Q K^T): against torch.softmax in fp64 (library
+    routine), rows sum to 1, and the sum of squares against numpy."""
+    rng = np.random.default_rng(3)
+    bh, L, d = 5, 48, 8
+    Q, K = rng.standard_normal((bh, L, d)), rng.standard_normal((bh, L, d))
+    scale = 1 / math.sqrt(d)
+    A, ss = oracle.score_mean(Q, K, scale)
+    ref = torch.softmax(torch.from_numpy(Q) @ torch.from_numpy(K).transpose(1, 2) * scale, dim=-1).mean(0).numpy()
+    assert np.abs(A - ref).max() < 1e-14
+    assert np.abs(A.sum(1) - 1).max() < 1e-12
+    assert abs(ss - float((ref ** 2).sum())) < 1e-12
+
+
+def test_transition_eq2_worked_numbers():
+    """Eq. 2 / Alg. 2 by hand: norms 3, 2.5, 2.2 -> distances 0.5, 0.3, |0.5 - 0.3| = 0.2."""
+    ok, d1, d2 = oracle.transition(9.0, 6.25, 4.84, 0.25)
+    assert ok and abs(d1 - 0.5) < 1e-12 and abs(d2 - 0.3) < 1e-12
+    ok, _, _ = oracle.transition(9.0, 6.25, 4.84, 0.15)
+    assert not ok
