@@ -217,6 +217,23 @@ SPION_API spion_status spion_step_host(const float *scores_host, const void *Q_h
                              spion_dtype dt, spion_softmax_mode mode, float scale, void *dev_arena,
                              size_t arena_bytes, int32_t *nnzb_host, void *stream);
 
+/* the dense-phase score matrix that feeds spion_pattern.
+ * A_dev[L][L] (fp32, row-major, caller-owned) = mean over the bh (batch, head)
+ * slices of softmax(scale Q K^T) — the attention score matrix averaged across
+ * heads and batch — and, if sumsq_dev != NULL, *sumsq_dev = sum of A^2
+ * (fp64), the square of the norm in Eq. 2 for Alg. 2's transition
+ * test (host side: |d_{i-1} - d_i| < alpha with d_i = |sqrt(s_{i-1})
+ * - sqrt(s_i)|).  Q, K: [bh][L][d] bf16 device, strides as spion_attn_fwd.
+ * Needs d = 64, L % 128 == 0, L <= 8192 (else UNSUPPORTED).  ws_dev: >=
+ * spion_score_mean_workspace_bytes(bh, L, d) bytes (a dense block pattern,
+ * forward scratch and the row normalisers).  Tensor cores: the dense forward
+ * gives every row's lse, then one pass forms each 128x128 tile of A over all
+ * bh in registers (no atomics on A). */
+SPION_API size_t spion_score_mean_workspace_bytes(int64_t bh, int32_t L, int32_t d);
+SPION_API spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, int32_t L, int32_t d,
+                             int64_t stride_bh, int64_t stride_l, float scale, void *ws_dev, size_t ws_bytes,
+                             float *A_dev, double *sumsq_dev, void *stream);
+
 /* Number of this library's kernels launched by this thread since process
  * start (host-side counter, for the bench's gpu_launches claim). */
 SPION_API int64_t spion_launch_count(void);

@@ -434,4 +434,62 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
     return SPION_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-1: dense-phase scores
+static size_t score_ws_layout(int64_t bh, int32_t L, size_t *o_pat, size_t *o_O, size_t *o_lse) {
+    const int n = L / 64;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += round_up(bytes, 256); return r; };
+    *o_pat = take((size_t)(n + 1) * 4 * 2 + (size_t)n * n * 4 * 2 + (size_t)n * n + 16 + 5 * 256 +
+                  spion_bsr_plan_bytes(L, 64));
+    *o_O = take((size_t)bh * L * 64 * 2);
+    *o_lse = take((size_t)bh * L * 4);
+    return o;
+}
+
+size_t spion_score_mean_workspace_bytes(int64_t bh, int32_t L, int32_t d) {
+    if (bh <= 0 || L <= 0 || d != 64 || L % 128) return 0;
+    size_t a, b, c;
+    return score_ws_layout(bh, L, &a, &b, &c);
+}
+
+spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, int32_t L, int32_t d,
+                              int64_t stride_bh, int64_t stride_l, float scale, void *ws_dev, size_t ws_bytes,
+                              float *A_dev, double *sumsq_dev, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!Q_dev || !K_dev || !A_dev || !ws_dev) return SPION_ERR_PARAM;
+    if (bh <= 0 || L <= 0 || d <= 0) return SPION_ERR_SHAPE;
+    if (d != 64 || L % 128 || L / 64 > 128 || bh > 65535) return SPION_ERR_UNSUPPORTED;
+    if (stride_l < d || stride_bh < (int64_t)stride_l * L || stride_l % 8 || stride_bh % 8) return SPION_ERR_ALIGN;
+    if (!aligned16(Q_dev) || !aligned16(K_dev) || !aligned16(A_dev) || !aligned16(ws_dev)) return SPION_ERR_ALIGN;
+    size_t o_pat, o_O, o_lse;
+    if (ws_bytes < score_ws_layout(bh, L, &o_pat, &o_O, &o_lse)) return SPION_ERR_WORKSPACE;
+    char *base = static_cast<char *>(ws_dev);
+    const int n = L / 64;
+    // a dense 64 x 64 block pattern (every block stored): the tensor-core forward in MASKED mode then
+    // returns every row's exact normaliser lse_i = ln sum_j exp(scale q_i . k_j)
+    spion_bsr bsr;
+    memset(&bsr, 0, sizeof(bsr));
+    size_t o = o_pat;
+    auto take = [&](size_t bytes) { char *r = base + o; o += round_up(bytes, 256); return r; };
+    bsr.nnzb_cap = n * n;
+    bsr.brow_ptr = reinterpret_cast<int32_t *>(take((size_t)(n + 1) * 4));
+    bsr.bcol_idx = reinterpret_cast<int32_t *>(take((size_t)n * n * 4));
+    bsr.bcol_ptr = reinterpret_cast<int32_t *>(take((size_t)(n + 1) * 4));
+    bsr.brow_idx = reinterpret_cast<int32_t *>(take((size_t)n * n * 4));
+    uint8_t *mask = reinterpret_cast<uint8_t *>(take((size_t)n * n));
+    bsr.nnzb = reinterpret_cast<int32_t *>(take(16));
+    bsr.plan_bytes = spion_bsr_plan_bytes(L, 64);
+    bsr.plan = take(bsr.plan_bytes);
+    SPION_CUDA_TRY(cudaMemsetAsync(mask, 1, (size_t)n * n, s));
+    spion_status st = spion_bsr_from_mask(mask, L, 64, &bsr, nullptr, stream);
+    if (st) return st;
+    bsr.mask = mask;
+    float *lse = reinterpret_cast<float *>(base + o_lse);
+    st = spion_attn_fwd(Q_dev, K_dev, K_dev, base + o_O, lse, bh, L, d, stride_bh, stride_l, SPION_BF16, &bsr,
+                        SPION_SOFTMAX_MASKED, scale, stream);
+    if (st) return st;
+    if (sumsq_dev) SPION_CUDA_TRY(cudaMemsetAsync(sumsq_dev, 0, sizeof(double), s));
+    return launch_score_mean(Q_dev, K_dev, lse, bh, L, stride_bh, stride_l, scale, A_dev, sumsq_dev, s);
+}
+
 }  // extern "C"

@@ -31,6 +31,13 @@ bool tc_supported(const AttnArgs &a, spion_dtype dt);
 spion_status launch_fwd_tc(const AttnArgs &a, cudaStream_t s);
 spion_status launch_bwd_tc(const AttnArgs &a, cudaStream_t s);
 
+// a TMA tensor map (CUtensorMap, 128-byte aligned) over [bh][L][64] bf16, 128B swizzle; attn_tc.cu
+bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l, int box_rows);
+
+// NEXT-1 dense-phase score mean; scores.cu
+spion_status launch_score_mean(const void *Q, const void *K, const float *lse, int64_t bh, int L, int64_t stride_bh,
+                               int64_t stride_l, float scale, float *A, double *sumsq, cudaStream_t s);
+
 // pattern kernels; pattern.cu
 size_t pattern_ws_bytes(int L, int block);
 spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos, int variant,

@@ -1384,6 +1384,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // [bh][L][64] bf16 viewed as a 3-D tensor; box = 64 x box_rows x 1, 128-byte swizzle
+bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l, int box_rows);
 static bool make_map(CUtensorMap *m, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l,
                      int box_rows) {
     auto enc = get_encode();
@@ -1396,6 +1397,10 @@ static bool make_map(CUtensorMap *m, const void *base, int L, int64_t bh, int64_
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l, int box_rows) {
+    return make_map(static_cast<CUtensorMap *>(map), base, L, bh, stride_bh, stride_l, box_rows);
 }
 
 bool tc_supported(const AttnArgs &a, spion_dtype dt) {

@@ -227,3 +227,30 @@ def attention(q, k, v, bp: BlockPattern, mode: str = "paper", scale: Optional[fl
 
 def launch_count() -> int:
     return int(N.lib().spion_launch_count())
+
+
+# ------------------------------------------------------------------ NEXT-1: dense-phase scores
+def score_mean(q: torch.Tensor, k: torch.Tensor, scale: Optional[float] = None, out: Optional[torch.Tensor] = None):
+    """A^s = mean over (batch, head) of softmax(scale q k^T) as fp32 [L][L], and sum(A^2)
+    (Eq. 2's squared norm) as a python float.  q, k: [bh][L][64] bf16 (device)."""
+    _require_cuda(q, k)
+    bh, L, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    lib = N.lib()
+    nb = lib.spion_score_mean_workspace_bytes(bh, L, d)
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=q.device)
+    A = out if out is not None else torch.empty((L, L), dtype=torch.float32, device=q.device)
+    ss = torch.zeros(1, dtype=torch.float64, device=q.device)
+    st = lib.spion_score_mean(_p(q), _p(k), bh, L, d, q.stride(0), q.stride(1), scale, _p(ws), nb, _p(A), _p(ss),
+                              _stream(q.device))
+    N.check(st, "spion_score_mean")
+    return A, float(ss.item())
+
+
+def transition(sumsq_im2: float, sumsq_im1: float, sumsq_i: float, alpha: float) -> bool:
+    """Alg. 2 with Eq. 2: distance_i = |sqrt(sum A_{i-1}^2) - sqrt(sum A_i^2)|; switch to the
+    sparse phase when |distance_{i-1} - distance_i| < alpha.  Host arithmetic on three norms."""
+    d1 = abs(math.sqrt(sumsq_im2) - math.sqrt(sumsq_im1))
+    d2 = abs(math.sqrt(sumsq_im1) - math.sqrt(sumsq_i))
+    return abs(d1 - d2) < alpha
+

@@ -270,3 +270,24 @@ def test_backward_deterministic():
     assert torch.equal(o, o2) and torch.equal(lse, lse2)
     for a, b in zip(g1, g2):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("bh,L", [(6, 256), (16, 1024), (3, 2048)])
+def test_score_mean_matches_oracle(bh, L):
+    """NEXT-1: the dense-phase score matrix A^s (mean over (batch, head) of softmax(scale Q K^T))
+    and its squared Frobenius norm against the fp64 oracle; rows of A^s sum to 1."""
+    spion = _spion()
+    d = 64
+    q, k, _, _ = synth.qkvdo(bh, L, d, seed=L + bh, dtype=torch.bfloat16)
+    A, ss = spion.score_mean(q.to(DEV), k.to(DEV))
+    A = A.cpu().numpy().astype(np.float64)
+    ref, ss_ref = oracle.score_mean(q.double().numpy(), k.double().numpy(), 1 / math.sqrt(d))
+    err = np.abs(A - ref).max()
+    assert err <= 1e-5 * np.abs(ref).max() + 1e-8, err  # measured ~7e-7 relative (fp32 S, ex2.approx)
+    assert np.abs(A.sum(1) - 1).max() < 1e-5
+    assert abs(ss - ss_ref) <= 1e-5 * ss_ref
+
+
+def test_transition_host_logic():
+    spion = _spion()
+    assert spion.transition(9.0, 6.25, 4.84, 0.25) and not spion.transition(9.0, 6.25, 4.84, 0.15)
