@@ -157,10 +157,11 @@ FULL = {
     "image": dict(L=1024, B=32, bh=256, alpha=75.0),
     "listops": dict(L=2048, B=64, bh=256, alpha=75.0),
     "text": dict(L=4096, B=64, bh=128, alpha=75.0),
+    "retrieval": dict(L=4096, B=64, bh=256, alpha=75.0),  # 2 towers x batch 16 x 8 heads
 }
 
 
-@pytest.mark.parametrize("cfg", ["image", "listops", "text"])
+@pytest.mark.parametrize("cfg", ["image", "listops", "text", "retrieval"])
 def test_full_size_sampled(cfg):
     """Bench launch configuration (pattern from synthetic scores, then fwd+bwd over every
     (batch, head)); the oracle recomputes sampled (batch, head) slices entirely."""
@@ -291,3 +292,18 @@ def test_score_mean_matches_oracle(bh, L):
 def test_transition_host_logic():
     spion = _spion()
     assert spion.transition(9.0, 6.25, 4.84, 0.25) and not spion.transition(9.0, 6.25, 4.84, 0.15)
+
+
+@pytest.mark.parametrize("cfg", ["image", "text"])
+def test_full_size_sampled_masked(cfg):
+    """The MASKED softmax (rows of P sum to 1, reading Q1) at full BASELINE sizes, sampled slices."""
+    spion = _spion()
+    c = FULL[cfg]
+    L, B, bh, d = c["L"], c["B"], c["bh"], 64
+    A = synth.lra_scores(L, B, seed=2)
+    bp = spion.pattern(A.to(DEV), B, filter=31, alpha=c["alpha"], sync=True)
+    fl, _, _ = oracle.pattern(A.numpy(), B, 31, c["alpha"])
+    q, k, v, do = synth.qkvdo(bh, L, d, seed=4048, dtype=torch.bfloat16)
+    outs = _run(q, k, v, do, bp, "masked", 1 / math.sqrt(d))
+    _compare(outs, q, k, v, do, fl, B, "masked", 1 / math.sqrt(d), [1, bh // 2, bh - 2], 2e-2, norm_tol=1e-2,
+             lse_tol=1e-3)

@@ -14,3 +14,4 @@ for c in image text; do
     -o $o/ncu_full_$c python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
 done
 ls -la $o
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $o/smoke.log 2>&1; tail -1 $o/smoke.log
