@@ -234,6 +234,25 @@ SPION_API spion_status spion_score_mean(const void *Q_dev, const void *K_dev, in
                              int64_t stride_bh, int64_t stride_l, float scale, void *ws_dev, size_t ws_bytes,
                              float *A_dev, double *sumsq_dev, void *stream);
 
+/* the sparse-MHA sub-layer around the attention (Alg. 5,
+ * P:655-674).  The projections Q,K,V = X W^{Q,K,V} (l.2) and S W^O (l.9) are plain
+ * GEMMs done by the caller (cuBLAS).
+ * spion_mha_heads: l.3 split / l.8 concatenate.  packed_dev: [batch][L][W][H][d]
+ * bf16 row-major (the projection output, W tensors side by side: W = 3 for
+ * Q|K|V, 1 for the concatenated heads); heads_dev: W tensors [batch*H][L][d],
+ * tensor w at element offset w*batch*H*L*d (the attention layout).  to_heads =
+ * 1: packed -> heads (split); 0: heads -> packed (concatenate, or the split's
+ * backward).  d % 8 == 0; 16-byte aligned pointers.
+ * spion_dropout_residual: l.9, out = e + dropout(y, p) (e != NULL), or the
+ * backward out = dropout(y, p) (e == NULL, y the incoming gradient), bf16, n
+ * elements; the keep mask is a counter-based hash of (seed, element index), so
+ * the backward with the same seed drops the same elements; kept values are
+ * scaled by 1/(1-p); 0 <= p < 1. */
+SPION_API spion_status spion_mha_heads(void *packed_dev, void *heads_dev, int64_t batch, int32_t L, int32_t W,
+                            int32_t H, int32_t d, int32_t to_heads, void *stream);
+SPION_API spion_status spion_dropout_residual(const void *y_dev, const void *e_dev, void *out_dev, int64_t n, float p,
+                                   uint64_t seed, void *stream);
+
 /* Number of this library's kernels launched by this thread since process
  * start (host-side counter, for the bench's gpu_launches claim). */
 SPION_API int64_t spion_launch_count(void);

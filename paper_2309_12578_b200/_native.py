@@ -42,6 +42,10 @@ EXPORTS = {
                                              ctypes.c_double, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p,
                                              ctypes.c_size_t, ctypes.POINTER(BSR), ctypes.c_void_p, ctypes.c_void_p]),
     "spion_pattern_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_mha_heads": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
+    "spion_dropout_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_float, ctypes.c_uint64, ctypes.c_void_p]),
     "spion_score_mean_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),
     "spion_score_mean": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t,

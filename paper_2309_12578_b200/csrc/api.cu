@@ -492,4 +492,24 @@ spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, 
     return launch_score_mean(Q_dev, K_dev, lse, bh, L, stride_bh, stride_l, scale, A_dev, sumsq_dev, s);
 }
 
+// ------------------------------------------------------------------ NEXT-4: sparse-MHA sub-layer
+spion_status spion_mha_heads(void *packed_dev, void *heads_dev, int64_t batch, int32_t L, int32_t W, int32_t H,
+                             int32_t d, int32_t to_heads, void *stream) {
+    if (!packed_dev || !heads_dev) return SPION_ERR_PARAM;
+    if (batch <= 0 || L <= 0 || W <= 0 || H <= 0 || d <= 0) return SPION_ERR_SHAPE;
+    if (d % 8) return SPION_ERR_UNSUPPORTED;
+    if (!aligned16(packed_dev) || !aligned16(heads_dev)) return SPION_ERR_ALIGN;
+    return launch_heads_permute(to_heads ? packed_dev : heads_dev, to_heads ? heads_dev : packed_dev, batch, L, W, H, d,
+                                to_heads, static_cast<cudaStream_t>(stream));
+}
+
+spion_status spion_dropout_residual(const void *y_dev, const void *e_dev, void *out_dev, int64_t n, float p,
+                                    uint64_t seed, void *stream) {
+    if (!y_dev || !out_dev) return SPION_ERR_PARAM;
+    if (n < 0) return SPION_ERR_SHAPE;
+    if (!(p >= 0.f && p < 1.f)) return SPION_ERR_PARAM;
+    if (n == 0) return SPION_OK;
+    return launch_dropout_residual(y_dev, e_dev, out_dev, n, p, seed, static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

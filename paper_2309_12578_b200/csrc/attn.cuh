@@ -38,6 +38,12 @@ bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_
 spion_status launch_score_mean(const void *Q, const void *K, const float *lse, int64_t bh, int L, int64_t stride_bh,
                                int64_t stride_l, float scale, float *A, double *sumsq, cudaStream_t s);
 
+// NEXT-4 sub-layer kernels; mha.cu
+spion_status launch_heads_permute(const void *src, void *dst, int64_t batch, int L, int W, int H, int d, int to_heads,
+                                  cudaStream_t s);
+spion_status launch_dropout_residual(const void *y, const void *e, void *out, int64_t n, float p, uint64_t seed,
+                                     cudaStream_t s);
+
 // pattern kernels; pattern.cu
 size_t pattern_ws_bytes(int L, int block);
 spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos, int variant,
