@@ -285,10 +285,16 @@ struct Arena {
 
 // spion_step_host pipelines the step over C contiguous (batch, head) chunks: the H2D copy of
 // chunk c+1, the attention of chunk c and the D2H copy of chunk c-1 overlap (copy engines in
-// both directions and the SMs busy at once)
-static int step_chunks(int64_t bh) {
-    for (int C : {8, 4, 2})
-        if (bh % C == 0 && bh / C >= 8) return C;
+// both directions and the SMs busy at once).  C (a power of two dividing bh, >= 8 (batch, head)
+// pairs per chunk) is the largest of 16/8/4/2 that keeps >= 4 MB per input tensor per chunk, capped
+// at 8 above 64 MB per tensor.  Measured on B200 (e2e ms/step, C = 4 / 8 / 16): Image 3.95 / 3.43 /
+// 3.79, ListOps 7.58 / 7.55 / 6.62, Text 8.55 / 8.68 / 7.92, Retrieval 15.26 / 14.88 / 15.65; the
+// step is bound by ~75 GB/s of combined H2D + D2H PCIe traffic, the chunking sets how much of it
+// overlaps.
+static int step_chunks(int64_t bh, size_t tensor_bytes) {
+    const int cmax = tensor_bytes > ((size_t)64 << 20) ? 8 : 16;
+    for (int C : {16, 8, 4, 2})
+        if (C <= cmax && bh % C == 0 && bh / C >= 8 && tensor_bytes / C >= ((size_t)4 << 20)) return C;
     return 1;
 }
 
@@ -310,7 +316,7 @@ static Arena arena_layout(int64_t bh, int32_t L, int32_t d, int32_t block, spion
     A.dK = take(t);
     A.dV = take(t);
     A.pws = take(pattern_ws_bytes(L, block));
-    const int C = step_chunks(bh);
+    const int C = step_chunks(bh, t);
     A.aws = take((size_t)C * spion_attn_workspace_bytes(bh / C, L, d, dt));  // one per bh chunk
     A.brow_ptr = take((size_t)(n + 1) * 4);
     A.bcol_idx = take((size_t)n * n * 4);
@@ -342,11 +348,11 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
     const size_t elt = dt == SPION_BF16 ? 2 : 4;
     const size_t t = (size_t)bh * L * d * elt;
     const int n = L / block;
-    const int C = step_chunks(bh);
+    const int C = step_chunks(bh, t);
     const int64_t bhc = bh / C;
     const size_t tc = t / C, lc = (size_t)bhc * L * 4, wsc = spion_attn_workspace_bytes(bhc, L, d, dt);
     // copy streams and events: created once per device and thread (the ABI's only state)
-    constexpr int MAXC = 8;
+    constexpr int MAXC = 16;
     struct Pipe {
         int dev = -1;
         cudaStream_t h2d = nullptr, d2h = nullptr;

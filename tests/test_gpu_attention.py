@@ -181,15 +181,17 @@ def test_full_size_sampled(cfg):
              lse_tol=1e-3)
 
 
-def test_step_host_matches_device_calls():
+@pytest.mark.parametrize("bh", [16, 256, 512])
+def test_step_host_matches_device_calls(bh):
     """spion_step_host (pipelined over (batch, head) chunks, host buffers) gives the same bytes as
-    spion_pattern + spion_attn_fwd + spion_attn_bwd on device buffers."""
+    spion_pattern + spion_attn_fwd + spion_attn_bwd on device buffers (bh = 16 / 256 / 512 run
+    as 1 / 8 / 16 chunks)."""
     import ctypes
 
     spion = _spion()
     from paper_2309_12578_b200 import _native as N
 
-    L, B, bh, d = 1024, 32, 16, 64
+    L, B, d = 1024, 32, 64
     A = synth.lra_scores(L, B, seed=5)
     q, k, v, do = synth.qkvdo(bh, L, d, seed=77, dtype=torch.bfloat16)
     scale = 1 / math.sqrt(d)
