@@ -47,7 +47,7 @@ def _compare(outs, q, k, v, do, fl, B, mode, scale, slices, tol, norm_tol=None, 
                 assert err / np.abs(ref).max() <= norm_tol, (name, b, err, np.abs(ref).max())
         fin = np.isfinite(lse_r)
         assert (np.isfinite(lse[b]) == fin).all()
-        if lse_tol is not None:
+        if lse_tol is not None and fin.any():
             assert np.abs(lse[b][fin] - lse_r[fin]).max() <= lse_tol
     return worst
 
@@ -150,6 +150,37 @@ def test_bf16_empty_rows():
     outs = _run(q, k, v, do, bp, "paper", 0.125)
     _compare(outs, q, k, v, do, fl, B, "paper", 0.125, range(2), 2e-2, norm_tol=1e-2, lse_tol=1e-3)
     assert (outs[0][:, 320:384] == 0).all()
+
+
+@pytest.mark.parametrize("mode", ["paper", "masked"])
+@pytest.mark.parametrize("B", [32, 64])
+def test_bf16_all_blocks_empty(mode, B):
+    """Degenerate pattern with no stored block (nnzb = 0): O = 0, lse = ln L (PAPER) / -inf
+    (MASKED), zero gradients - the tcgen05 kernels' empty-plan path, against the oracle."""
+    spion = _spion()
+    L, d = 512, 64
+    fl = np.zeros((L // B, L // B), dtype=np.uint8)
+    bp = spion.bsr_from_mask(torch.from_numpy(fl).to(DEV), L, B)
+    assert bp.nnzb == 0
+    q, k, v, do = synth.qkvdo(3, L, d, seed=9, dtype=torch.bfloat16)
+    outs = _run(q, k, v, do, bp, mode, 0.125)
+    _compare(outs, q, k, v, do, fl, B, mode, 0.125, range(3), 0.0, lse_tol=1e-3)
+    for x in (outs[0], outs[2], outs[3], outs[4]):
+        assert (x == 0).all()
+
+
+def test_attention_rejects_bad_shapes():
+    """bh = 0 and d beyond the supported head widths are refused with SPION_ERR_SHAPE (raised by
+    the binding), not silently skipped."""
+    spion = _spion()
+    from paper_2309_12578_b200 import _native as N
+    L, B = 256, 32
+    fl = synth.syn_mask(L // B, 0.3, seed=1)
+    bp = spion.bsr_from_mask(torch.from_numpy(fl).to(DEV), L, B)
+    for bh, d in ((0, 64), (2, 256)):
+        q = torch.zeros((bh, L, d), dtype=torch.bfloat16, device=DEV)
+        with pytest.raises(Exception):
+            spion.attn_fwd(q, q, q, bp, "paper", 0.125)
 
 
 # ------------------------------------------ full BASELINE sizes, sampled slices
