@@ -254,7 +254,10 @@ static spion_status k1_launch(const float *scores, const K1Geom &g, unsigned lon
 }
 
 // ---------------------------------------------------------------- K2
-static constexpr int K2_THREADS = 1024;
+#ifndef SPION_K2_THREADS
+#define SPION_K2_THREADS 1024
+#endif
+static constexpr int K2_THREADS = SPION_K2_THREADS;
 static constexpr int K2_MAXN = 128;  // n = L/B <= 128: one row of the block grid is 4 x 32 bits
 
 // 128-bit row bitboard (bit c = block column c)
@@ -290,7 +293,9 @@ __device__ __forceinline__ void b_store(unsigned *w, Bits a) {
 }
 __device__ __forceinline__ unsigned b_get(const unsigned *w, int c) { return (w[c >> 5] >> (c & 31)) & 1u; }
 
-// k-th smallest (0-based) of v[0..N) by MSD radix selection, 8-bit digits.
+// k-th smallest (0-based) of v[0..N) by MSD radix selection, 8-bit digits.  Once the digit
+// bucket holding the k-th value has <= 32 members, they are compacted and one warp ranks them
+// directly (the remaining low digits would each cost a full histogram pass).
 __device__ long long block_select_kth(const long long *v, int N, long long k, unsigned int *hist,
                                       long long *bc, int top_shift) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -313,13 +318,40 @@ __device__ long long block_select_kth(const long long *v, int N, long long k, un
             long long below = ex;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
-                if (k >= below && k < below + (long long)c[t]) { bc[0] = lane * 8 + t; bc[1] = below; }
+                if (k >= below && k < below + (long long)c[t]) { bc[0] = lane * 8 + t; bc[1] = below; bc[2] = c[t]; }
                 below += c[t];
             }
+            if (lane == 0) bc[3] = 0;
         }
         __syncthreads();
         prefix |= ((unsigned long long)bc[0]) << shift;
         k -= bc[1];
+        const long long cnt = bc[2];
+        if (shift > 0 && cnt <= 32) {
+            // compact the bucket's members (hist[0..32) reused as the list) and rank them in one warp
+            const unsigned long long m = ~0ull << shift;
+            unsigned long long *cand = reinterpret_cast<unsigned long long *>(hist);
+            __syncthreads();
+            for (int i = tid; i < N; i += blockDim.x) {
+                const unsigned long long x = (unsigned long long)v[i];
+                if ((x & m) == prefix) cand[atomicAdd(reinterpret_cast<unsigned long long *>(&bc[3]), 1ull)] = x;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const unsigned long long x = lane < cnt ? cand[lane] : ~0ull;
+                int less = 0, eq_before = 0;
+                for (int j = 0; j < (int)cnt; ++j) {
+                    const unsigned long long y = __shfl_sync(0xffffffffu, x, j);
+                    less += y < x;
+                    eq_before += (y == x) && (j < lane);
+                }
+                if (lane < cnt && less + eq_before == k) bc[0] = (long long)x;
+            }
+            __syncthreads();
+            const long long r = bc[0];
+            __syncthreads();
+            return r;
+        }
         __syncthreads();
     }
     return (long long)prefix;
@@ -545,7 +577,9 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
         const unsigned long long all = s_red[0];
         const int topbit = all ? 63 - __clzll((long long)all) : 0;
         const int top_shift = (topbit / 8) * 8;
+        k2_stamp(a, 12);
         const long long v_lo = block_select_kth(s_pool, N, a.lo, hist, bc, top_shift);
+        k2_stamp(a, 13);
         if (a.kind == SPION_TH_QUANTILE_LINEAR && a.frac_pos) {
             // t = v[lo] + frac (v[lo+1] - v[lo]) with 0 < frac < 1: x > t <=> x >= v[lo+1] if the
             // gap is positive, else x > v[lo]
@@ -555,8 +589,14 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
                 long long x = s_pool[i];
                 if (x <= v_lo) ++le; else mn = min(mn, (unsigned long long)x);
             }
-            atomicAdd(&s_le, le);
-            atomicMin(&s_red[1], mn);
+            for (int o = 16; o > 0; o >>= 1) {
+                le += __shfl_xor_sync(0xffffffffu, le, o);
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            }
+            if (lane == 0) {
+                atomicAdd(&s_le, le);
+                atomicMin(&s_red[1], mn);
+            }
             __syncthreads();
             const bool tie = (long long)s_le >= a.lo + 2;
             T = tie ? v_lo : (long long)s_red[1] - 1;

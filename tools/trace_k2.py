@@ -18,6 +18,7 @@ for L, B in [(1024, 32), (2048, 64), (4096, 64)]:
     d = np.diff(t[:7]) / 1000
     print(L, B, "K2 phases us: load %.2f thresh %.2f edges %.2f flood %.2f fl %.2f bsr+plan %.2f total %.2f" % (*d, (t[6] - t[0]) / 1000))
     seq = [t[5], t[7], t[8], t[9], t[10], t[11], t[6]]
+    print("   thresh: or %.2f select %.2f tie %.2f" % tuple(np.diff([buf[1], buf[12], buf[13], buf[2]]) / 1000))
     print("   bsr+plan: colw %.2f cnt+scan %.2f ptr+idx %.2f mask %.2f plan-cnt+scan %.2f plan-lists %.2f" % tuple(np.diff(seq) / 1000))
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
