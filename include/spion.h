@@ -203,7 +203,8 @@ SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, cons
  * pinned for asynchronous copies.  dev_arena: caller-owned device memory of
  * >= spion_step_arena_bytes(...) bytes.  Synchronises `stream` and returns
  * nnzb in *nnzb_host (may be NULL).
- * The (batch, head) range is processed in up to 8 contiguous chunks, pipelined:
+ * The (batch, head) range is processed in up to 16 contiguous chunks (>= 8 pairs and >= 4 MB per
+ * input tensor each), pipelined:
  * the H2D copy of chunk c+1, the attention of chunk c (on `stream`) and the D2H
  * copy of chunk c-1 overlap, on two copy streams the library creates once per
  * device and host thread (with their events: the ABI's only internal state).

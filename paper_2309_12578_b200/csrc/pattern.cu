@@ -73,8 +73,10 @@ struct K1Cfg {
     static __device__ __forceinline__ int ppidx(int pos) { return (pos % CH) * 32 + pos / CH; }
 };
 
+// K4 = 4 (every LRA shape): registers capped for 3 resident CTAs per SM (78 regs, no spill;
+// uncapped it took 96+ and 2 CTAs per SM: -2 us at L = 2048/4096).  The wider windows would spill.
 template <int K4>
-__global__ void __launch_bounds__(K1_WARPS * 32)
+__global__ void __launch_bounds__(K1_WARPS * 32, K4 == 4 ? 3 : 1)
 pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *__restrict__ pool,
                     int *__restrict__ flags) {
     using C = K1Cfg<K4>;
