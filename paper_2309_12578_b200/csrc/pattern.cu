@@ -26,8 +26,8 @@ namespace spion {
 #define SPION_HEAVY_FIRST 1
 #endif
 // ---------------------------------------------------------------- K1
-#ifndef SPION_K1_CTAS  // split a block row's source rows across CTAs until the grid has this many
-#define SPION_K1_CTAS (4 * 148)
+#ifndef SPION_K1_PER_SM  // resident K1 CTAs per SM (register cap of the K4 = 4 instantiation)
+#define SPION_K1_PER_SM 3
 #endif
 static constexpr int K1_WARPS = 8;
 static constexpr int K1_MAXP = 2;  // (target row, column) pairs per lane
@@ -52,8 +52,20 @@ static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
     const int n_cc = (n + jmax - 1) / jmax;
     g.JC = (n + n_cc - 1) / n_cc;
     g.n_cc = (n + g.JC - 1) / g.JC;
-    int rs = 1;  // split the rows of a block row until the grid covers the GPU a few times
-    while (g.n_cc * n * rs < SPION_K1_CTAS && B / (2 * rs) >= 2 * K1_WARPS) rs *= 2;
+    // split the rows of a block row over rs CTAs (>= 2 rows per warp each): the rs with the best
+    // wave efficiency (waves / ceil(waves)) over the resident CTA slots, the smallest on ties
+    static int slots = 0;
+    if (!slots) {
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        slots = SPION_K1_PER_SM * sms;
+    }
+    int rs = 1;
+    double best = -1.0;
+    for (int r = 1; r == 1 || B / (2 * r) >= 2 * K1_WARPS; r *= 2) {
+        const double w = (double)g.n_cc * n * r / slots, eff = w / ceil(w);
+        if (eff > best + 1e-9) { best = eff; rs = r; }
+    }
     g.RP = (B + rs - 1) / rs;
     return true;
 }
@@ -76,7 +88,7 @@ struct K1Cfg {
 // K4 = 4 (every LRA shape): registers capped for 3 resident CTAs per SM (78 regs, no spill;
 // uncapped it took 96+ and 2 CTAs per SM: -2 us at L = 2048/4096).  The wider windows would spill.
 template <int K4>
-__global__ void __launch_bounds__(K1_WARPS * 32, K4 == 4 ? 3 : 1)
+__global__ void __launch_bounds__(K1_WARPS * 32, K4 == 4 ? SPION_K1_PER_SM : 1)
 pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *__restrict__ pool,
                     int *__restrict__ flags) {
     using C = K1Cfg<K4>;
@@ -147,21 +159,21 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
         // pass 1 over the lane chunk: tot = sum q, ppl = sum_e q_e (CH-1-e) (the chunk's P-sum share)
         unsigned lo[C::HOLD ? CH : 1];
         unsigned long long tot = 0, ppl = 0;
-        bool fast = true;  // every element in [0, 1)
+        unsigned mxb = 0;  // max of the bit patterns: every element in [0, 1) <=> mxb < bits(1.0f)
 #pragma unroll
         for (int i = 0; i < K4; ++i) {
             const float4 f = stage[C::own4(lane, i)];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const float a = elem(f, t);
-                fast = fast && (a >= 0.f) && (a < 1.f);
+                mxb = max(mxb, __float_as_uint(a));
                 const unsigned l = lo32(a);
                 if constexpr (C::HOLD) lo[4 * i + t] = l;
                 tot += l;
                 ppl += (unsigned long long)l * (unsigned)(CH - 1 - (4 * i + t));
             }
         }
-        const bool slow = !__all_sync(0xffffffffu, fast);
+        const bool slow = !__all_sync(0xffffffffu, mxb < 0x3f800000u);
         unsigned fix = 0;  // HOLD: bit e set where q_e = 2^32 (a = 1): one more than the saturated u32
         if (slow) {
 #pragma unroll
@@ -184,6 +196,14 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
         const unsigned long long off1 = warp_excl_scan_u64(tot, lane);
         const unsigned long long off2 = warp_excl_scan_u64((unsigned long long)CH * off1 + ppl, lane);
         unsigned long long run = off1, run2 = off2;
+        if (C::HOLD && !slow) {  // warp-uniform common case: no a = 1 fix-ups
+#pragma unroll
+            for (int e = 0; e < CH; ++e) {
+                pp[e * 32 + lane] = run2;
+                run2 += run;
+                run += (unsigned long long)lo[C::HOLD ? e : 0];
+            }
+        } else
 #pragma unroll
         for (int i = 0; i < K4; ++i) {
             float4 f;
