@@ -145,6 +145,7 @@ struct TcParams {
     int off_order;                  // tiles in descending work order
     int off_sched;                  // plan words [off_sched] item counter, [off_sched+1] done counter
     int off_heavy;                  // plan word: number of heavy tiles (scheduled first)
+    int off_perm;                   // column tiles: plan word offset of bperm (slot -> block column)
     int G;                          // (batch, head) chunk of the scheduling order
     int S;                          // slots per tile
     unsigned long long *trace;      // optional event trace of CTA 0 (SPION_TRACE=1), else null
@@ -191,6 +192,7 @@ struct Sched {
     uint64_t *full, *empty;  // [4] each
 };
 static constexpr int TAB_ORDER = 8, TAB_PTR = TAB_ORDER + SCHED_CAP, TAB_RC = TAB_PTR + SCHED_CAP + 8;
+static constexpr int TAB_PERM = TAB_RC;  // column-tile kernels (no block-row counts): plan bperm
 static constexpr int SCHED_TAB = TAB_RC + SCHED_CAP;
 static constexpr int SCHED_BYTES = (32 + 2 * 4 * SCHED_CAP + SCHED_TAB) * 4;
 
@@ -213,6 +215,8 @@ __device__ __forceinline__ void sched_load_tables(const Sched &sc, const TcParam
     for (int i = threadIdx.x; i <= p.ntiles; i += blockDim.x) sc.tab[TAB_PTR + i] = p.plan[p.off_ptr + i];
     if (want_rc)
         for (int i = threadIdx.x; i < p.n; i += blockDim.x) sc.tab[TAB_RC + i] = p.brow_ptr[i + 1] - p.brow_ptr[i];
+    else if (p.off_perm)  // column tiles: the slot -> block column table in the same area
+        for (int i = threadIdx.x; i < p.ntiles * p.S; i += blockDim.x) sc.tab[TAB_PERM + i] = p.plan[p.off_perm + i];
 }
 
 // `consumers` warps release each slot: the MMA warp and every softmax warp
@@ -1075,9 +1079,19 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 if (nk >= 2) mbar_wait(kv_empty + kb, ((nk >> 1) - 1) & 1);
                 if (lane == 0) tr.ev(2);
                 if (elect_one()) {
-                    mbar_arrive_expect_tx(kv_full + kb, 32768);
-                    tma_load_3d(sKV + kb * 32768, &tmK, kv_full + kb, 0, t * 128, bh);
-                    tma_load_3d(sKV + kb * 32768 + 16384, &tmV, kv_full + kb, 0, t * 128, bh);
+                    // the tile's S block columns (plan bperm: heavy columns grouped), one B-row box
+                    // each at slot offset s*B rows (same SW128 layout as one 128-row box); empty
+                    // slots are not loaded (their rows are masked in every entry, never stored)
+                    const int *pm = sc.tab + TAB_PERM + t * p.S;
+                    int nval = 0;
+                    for (int sl = 0; sl < p.S; ++sl) nval += pm[sl] < p.n;
+                    mbar_arrive_expect_tx(kv_full + kb, (uint32_t)nval * 2 * B * 128);
+                    for (int sl = 0; sl < p.S; ++sl) {
+                        const int c = pm[sl];
+                        if (c >= p.n) continue;
+                        tma_load_3d(sKV + kb * 32768 + sl * B * 128, &tmK, kv_full + kb, 0, c * B, bh);
+                        tma_load_3d(sKV + kb * 32768 + 16384 + sl * B * 128, &tmV, kv_full + kb, 0, c * B, bh);
+                    }
                 }
                 __syncwarp();
                 ++nk;
@@ -1222,8 +1236,13 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 mbar_wait(staged + sb, (ns >> 1) & 1);
                 ++ns;
                 if (lane == 0) {
-                    tma_store_3d(&tmdK, sKV + sb * 32768, 0, t * 128, bh);
-                    tma_store_3d(&tmdV, sKV + sb * 32768 + 16384, 0, t * 128, bh);
+                    const int *pm = sc.tab + TAB_PERM + t * p.S;
+                    for (int sl = 0; sl < p.S; ++sl) {
+                        const int c = pm[sl];
+                        if (c >= p.n) continue;
+                        tma_store_3d(&tmdK, sKV + sb * 32768 + sl * B * 128, 0, c * B, bh);
+                        tma_store_3d(&tmdV, sKV + sb * 32768 + 16384 + sl * B * 128, 0, c * B, bh);
+                    }
                     bulk_commit();
                     bulk_wait_read0();
                     mbar_arrive(kv_empty + sb);
@@ -1448,6 +1467,7 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     p.off_order = (int)(rows ? pl.forder : pl.border);
     p.off_sched = 8 + 2 * which;
     p.off_heavy = rows ? 5 : 6;
+    p.off_perm = rows ? 0 : (int)pl.bperm;
     const int grid = ctas * num_sms();
     int G = (2 * grid + pl.ntiles - 1) / pl.ntiles;
     if (G < 1) G = 1;
@@ -1504,19 +1524,17 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
         SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dkv_smem<B>()));
         attr = true;
     }
-    CUtensorMap mq128, mdo128, mo128, mkB, mvB, mk128, mv128, mqB, mdoB, mdq128, mdk128, mdv128;
+    CUtensorMap mq128, mdo128, mo128, mkB, mvB, mqB, mdoB, mdq128, mdkB, mdvB;
     if (!make_map(&mq128, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mdo128, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mo128, a.O, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mkB, a.K, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
         !make_map(&mvB, a.V, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
-        !make_map(&mk128, a.K, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
-        !make_map(&mv128, a.V, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mqB, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
         !make_map(&mdoB, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
         !make_map(&mdq128, a.dQ, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
-        !make_map(&mdk128, a.dK, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
-        !make_map(&mdv128, a.dV, a.L, a.bh, a.stride_bh, a.stride_l, 128))
+        !make_map(&mdkB, a.dK, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
+        !make_map(&mdvB, a.dV, a.L, a.bh, a.stride_bh, a.stride_l, B))
         return SPION_ERR_CUDA;
     // 1) dQ (row tiles) and D = rowsum(dO * O)
     TcParams p = base_params(a, 1, Cfg<B>::DQ_CTAS);
@@ -1534,7 +1552,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     q.dK = a.dK;
     q.dV = a.dV;
     attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), bwd_threads(Cfg<B>::DKV_MW, Cfg<B>::DKV_NSW), dkv_smem<B>(), s>>>(
-        mk128, mv128, mqB, mdoB, mdk128, mdv128, q);
+        mkB, mvB, mqB, mdoB, mdkB, mdvB, q);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }

@@ -22,6 +22,9 @@
 
 namespace spion {
 
+#ifndef SPION_GROUP_HEAVY  // plan: heavy block columns grouped into the same column tiles
+#define SPION_GROUP_HEAVY 1
+#endif
 #ifndef SPION_HEAVY_FIRST  // plan: tiles with > 2x the mean work scheduled first (attention tail)
 #define SPION_HEAVY_FIRST 1
 #endif
@@ -409,6 +412,7 @@ struct K2Scratch {
     unsigned *colw;  // [K2_MAXN][4] column bitboards (bit r of column c)
     int *cnt;        // [2 * K2_MAXN]
     int *off;        // [2 * (K2_MAXN + 1)]
+    int *perm;       // [K2_MAXN + 32] column-tile order (plan bperm)
 };
 
 // exclusive scans of cnt[0..m) and cnt[m..2m) into off[0..m] and off[m+1..2m+1]; warp 0 only
@@ -477,13 +481,36 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
     int *plan = a.plan;
     __syncthreads();
     k2_stamp(a, 10);
+    // column-tile order: the heavy block columns (more than twice the mean count; the columns of
+    // vertical stripes, whose row sets overlap) first, then the rest, each ascending.  Tiling
+    // consecutive columns would pair a stripe column with band columns, so most of the stripe's
+    // union entries would carry one useful slot of S.  Row tiles keep the natural order.
+    if (tid < 32) {
+        const long long nnzb = sc.off[n];
+        int pos = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int c0 = 0; c0 < n; c0 += 32) {
+                const int c = c0 + tid;
+                const bool hv = c < n && SPION_GROUP_HEAVY && (long long)sc.cnt[n + c] * n > 2 * nnzb;
+                const bool take = c < n && (hv == (pass == 0));
+                const unsigned bl = __ballot_sync(0xffffffffu, take);
+                if (take) sc.perm[pos + __popc(bl & ((1u << tid) - 1u))] = c;
+                pos += __popc(bl);
+            }
+            if (pass == 0 && tid == 0) plan[7] = pos;
+        }
+        for (int i = n + tid; i < pl.ntiles * pl.S; i += 32) sc.perm[i] = n;
+        __syncwarp();
+        for (int i = tid; i < pl.ntiles * pl.S; i += 32) plan[pl.bperm + i] = sc.perm[i];
+    }
+    __syncthreads();
     for (int t = tid; t < 2 * pl.ntiles; t += nthr) {
         const bool fwd = t < pl.ntiles;
         const int tt = fwd ? t : t - pl.ntiles;
         const unsigned *src = fwd ? sc.flw : sc.colw;
         Bits u{0ull, 0ull};
         for (int s = 0; s < pl.S; ++s) {
-            const int r = tt * pl.S + s;
+            const int r = fwd ? tt * pl.S + s : sc.perm[tt * pl.S + s];
             if (r < n) u = b_or(u, b_load(src + r * 4));
         }
         sc.cnt[t] = b_popc(u);
@@ -511,7 +538,7 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
             plan[0] = n; plan[1] = pl.S; plan[2] = pl.ntiles;
             plan[3] = sc.off[pl.ntiles];
             plan[4] = sc.off[2 * pl.ntiles + 1];
-            for (int w = 5; w < 16; ++w) plan[w] = 0;  // scheduler counters start at zero
+            for (int w = 8; w < 16; ++w) plan[w] = 0;  // scheduler counters start at zero
             plan[5] = heavy[0];  // heavy row tiles (a prefix of the descending work order)
             plan[6] = heavy[1];  // heavy column tiles
         }
@@ -538,7 +565,7 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
         const int wsel = lane >> 3, sh = (lane & 7) * 4;
         unsigned nib = 0;
         for (int sl = 0; sl < pl.S; ++sl) {
-            const int r = tt * pl.S + sl;
+            const int r = fwd ? tt * pl.S + sl : sc.perm[tt * pl.S + sl];
             if (r < n) nib |= (src[r * 4 + wsel] >> sh) & 15u;
         }
         int o = sc.off[(fwd ? 0 : pl.ntiles + 1) + tt] + warp_excl_scan_i32(__popc(nib), lane);
@@ -550,7 +577,7 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
             const int j = 4 * lane + k;
             int m = 0;
             for (int sl = 0; sl < pl.S; ++sl) {
-                const int r = tt * pl.S + sl;
+                const int r = fwd ? tt * pl.S + sl : sc.perm[tt * pl.S + sl];
                 if (r < n) m |= (int)((src[r * 4 + wsel] >> (sh + k)) & 1u) << sl;
             }
             col[o] = j;
@@ -576,6 +603,7 @@ __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) 
     sc.cnt = reinterpret_cast<int *>(sc.colw + k2_bits_words());
     sc.off = sc.cnt + 2 * K2_MAXN + 8;
     unsigned int *hist = reinterpret_cast<unsigned int *>(sc.off + 2 * (K2_MAXN + 1) + 8);
+    sc.perm = reinterpret_cast<int *>(hist + 256);
     __shared__ long long bc[4];
     __shared__ unsigned long long s_red[2];
     __shared__ unsigned int s_le;
@@ -743,6 +771,7 @@ __global__ void __launch_bounds__(K2_THREADS) bsr_from_mask_kernel(const uint8_t
     sc.colw = sc.flw + k2_bits_words();
     sc.cnt = reinterpret_cast<int *>(sc.colw + k2_bits_words());
     sc.off = sc.cnt + 2 * K2_MAXN + 8;
+    sc.perm = sc.off + 2 * (K2_MAXN + 1) + 8 + 256;
     __shared__ int s_bad;
     if (tid == 0) s_bad = 0;
     __syncthreads();
@@ -771,7 +800,7 @@ size_t pattern_ws_bytes(int L, int block) {
 static size_t k2_smem_bytes(int n, bool with_pool) {
     size_t b = with_pool ? (((size_t)n * n + 1) & ~(size_t)1) * 8 + 4 * (size_t)k2_bits_words() * 4 : 0;  // pool, gt/dn/rt/dg
     b += 2 * (size_t)k2_bits_words() * 4;                                             // fl, columns
-    b += (2 * K2_MAXN + 8) * 4 + (2 * (K2_MAXN + 1) + 8) * 4 + 256 * 4 + 64;
+    b += (2 * K2_MAXN + 8) * 4 + (2 * (K2_MAXN + 1) + 8) * 4 + 256 * 4 + (K2_MAXN + 32) * 4 + 64;
     return b;
 }
 

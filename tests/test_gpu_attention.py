@@ -252,8 +252,9 @@ def test_step_host_matches_device_calls(bh):
 @pytest.mark.parametrize("L,B", [(1024, 32), (2048, 64), (4096, 64)])
 def test_plan_matches_host_recomputation(L, B):
     """The attention work plan built by the pattern kernel (slot tiles of S = 128/B block rows /
-    columns, union lists with slot masks, descending-work order, heavy-tile counts) equals a
-    plain host recomputation from the block mask."""
+    columns, union lists with slot masks, descending-work order, heavy-tile counts, and the
+    column-tile order that groups the heavy block columns - more than twice the mean count -
+    ahead of the rest) equals a plain host recomputation from the block mask."""
     spion = _spion()
     A = synth.lra_scores(L, B, seed=3)
     bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
@@ -270,16 +271,25 @@ def test_plan_matches_host_recomputation(L, B):
     fcol = border + nt
     fmsk, brow = fcol + cap, fcol + 2 * cap
     bmsk = brow + cap
+    bperm = bmsk + cap
     assert list(plan[:3]) == [n, S, nt]
-    for which, (ptr, order, col, msk, grid) in enumerate(((fptr, forder, fcol, fmsk, fl), (bptr, border, brow, bmsk, fl.T))):
+    colcnt = fl.sum(0)
+    heavy = [c for c in range(n) if colcnt[c] * n > 2 * fl.sum()]
+    want_perm = heavy + [c for c in range(n) if c not in heavy] + [n] * (nt * S - n)
+    assert list(plan[bperm:bperm + nt * S]) == want_perm
+    assert plan[7] == len(heavy)
+    row_order = list(range(n)) + [n] * (nt * S - n)
+    for which, (ptr, order, col, msk, grid, perm) in enumerate(((fptr, forder, fcol, fmsk, fl, row_order),
+                                                               (bptr, border, brow, bmsk, fl.T, want_perm))):
         cnts = []
         for t in range(nt):
-            rows = grid[t * S:(t + 1) * S]
+            slots = perm[t * S:(t + 1) * S]
+            rows = np.stack([grid[r] if r < n else np.zeros(n, dtype=bool) for r in slots])
             union = np.nonzero(rows.any(0))[0]
             beg, end = plan[ptr + t], plan[ptr + t + 1]
             assert end - beg == len(union)
             assert (plan[col + beg:col + end] == union).all()
-            want_m = [sum(int(rows[s, j]) << s for s in range(rows.shape[0])) for j in union]
+            want_m = [sum(int(rows[s, j]) << s for s in range(S)) for j in union]
             assert list(plan[msk + beg:msk + end]) == want_m
             cnts.append(len(union))
         want_order = sorted(range(nt), key=lambda t: (-cnts[t], t))
