@@ -92,7 +92,7 @@ struct PlanLayout {
     int n, S, ntiles;
     // header words: [0] n [1] S [2] ntiles [3] fwd entries [4] bwd entries
     //               [5] heavy row tiles [6] heavy column tiles (prefixes of the work orders)
-    //               [7] heavy block columns grouped first in the column-tile order (bperm)
+    //               [7] heavy block columns (> 2x the mean count; a prefix of bperm)
     //               [8] fwd item counter [9] fwd done [10] bwd item counter [11] bwd done
     size_t fptr, bptr, forder, border, fcol, fmsk, brow, bmsk, bperm, words;
     __host__ __device__ PlanLayout(int n_, int block) {

@@ -253,8 +253,7 @@ def test_step_host_matches_device_calls(bh):
 def test_plan_matches_host_recomputation(L, B):
     """The attention work plan built by the pattern kernel (slot tiles of S = 128/B block rows /
     columns, union lists with slot masks, descending-work order, heavy-tile counts, and the
-    column-tile order that groups the heavy block columns - more than twice the mean count -
-    ahead of the rest) equals a plain host recomputation from the block mask."""
+    column-tile order: block columns by descending count, stable) equals a plain host recomputation from the block mask."""
     spion = _spion()
     A = synth.lra_scores(L, B, seed=3)
     bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
@@ -274,10 +273,9 @@ def test_plan_matches_host_recomputation(L, B):
     bperm = bmsk + cap
     assert list(plan[:3]) == [n, S, nt]
     colcnt = fl.sum(0)
-    heavy = [c for c in range(n) if colcnt[c] * n > 2 * fl.sum()]
-    want_perm = heavy + [c for c in range(n) if c not in heavy] + [n] * (nt * S - n)
+    want_perm = sorted(range(n), key=lambda c: (-colcnt[c], c)) + [n] * (nt * S - n)
     assert list(plan[bperm:bperm + nt * S]) == want_perm
-    assert plan[7] == len(heavy)
+    assert plan[7] == sum(1 for c in range(n) if colcnt[c] * n > 2 * fl.sum())
     row_order = list(range(n)) + [n] * (nt * S - n)
     for which, (ptr, order, col, msk, grid, perm) in enumerate(((fptr, forder, fcol, fmsk, fl, row_order),
                                                                (bptr, border, brow, bmsk, fl.T, want_perm))):
