@@ -428,6 +428,7 @@ __device__ void scan2(const int *cnt, int *off, int m) {
         for (int t = 0; t < per; ++t) { const int r = lane * per + t; if (r < m) { o[r] = ex; ex += c[r]; } }
         if (lane == 31) o[m] = ex;
     }
+    __syncwarp();  // lanes read offsets written by other lanes (racecheck)
 }
 
 // Block-CSR / CSC / plan from the row bitboards sc.flw (all threads of the CTA).
