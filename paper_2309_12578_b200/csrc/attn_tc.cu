@@ -55,7 +55,7 @@
 #define SPION_DBG_NOSOFTMAX 0
 #endif
 #ifndef SPION_HEAVY_AHEAD  // heavy tiles are scheduled this many (batch, head) chunks ahead
-#define SPION_HEAVY_AHEAD 2
+#define SPION_HEAVY_AHEAD 3
 #endif
 #ifndef SPION_NSW  // 1: one S-MMA warp per buffer where one CTA owns the SM (0: a single S-MMA warp)
 #define SPION_NSW 0
