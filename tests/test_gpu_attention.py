@@ -140,6 +140,25 @@ def test_bf16_parity(L, B, d, bh, density, mode):
     _compare(outs, q, k, v, do, fl, B, mode, scale, range(bh), 2e-2, norm_tol=1e-2, lse_tol=1e-3)
 
 
+@pytest.mark.parametrize("L,B,cols", [(1024, 32, (3, 17, 30)), (1088, 64, (0, 9, 16)), (512, 32, (15,))])
+def test_bf16_stripe_columns(L, B, cols):
+    """Band + full vertical stripes (the LRA-like structure): the dK/dV column tiles take the
+    block columns in count order, so stripe columns share tiles and are loaded / stored as
+    separate B-row boxes at their own coordinates (ragged tails included)."""
+    spion = _spion()
+    n = L // B
+    fl = np.zeros((n, n), dtype=np.uint8)
+    for i in range(n):
+        fl[i, max(0, i - 1):i + 2] = 1
+    for c in cols:
+        fl[:, c] = 1
+    bp = spion.bsr_from_mask(torch.from_numpy(fl).to(DEV), L, B)
+    q, k, v, do = synth.qkvdo(2, L, 64, seed=L + B, dtype=torch.bfloat16)
+    for mode in ("paper", "masked"):
+        outs = _run(q, k, v, do, bp, mode, 0.125)
+        _compare(outs, q, k, v, do, fl, B, mode, 0.125, range(2), 2e-2, norm_tol=1e-2, lse_tol=1e-3)
+
+
 def test_bf16_empty_rows():
     spion = _spion()
     L, B, d = 512, 64, 64
