@@ -54,8 +54,11 @@
 #ifndef SPION_DBG_NOSOFTMAX
 #define SPION_DBG_NOSOFTMAX 0
 #endif
+#ifndef SPION_G_MULT  // scheduling chunk: ~this many work items per CTA
+#define SPION_G_MULT 4
+#endif
 #ifndef SPION_HEAVY_AHEAD  // heavy tiles are scheduled this many (batch, head) chunks ahead
-#define SPION_HEAVY_AHEAD 3
+#define SPION_HEAVY_AHEAD 2
 #endif
 #ifndef SPION_NSW  // 1: one S-MMA warp per buffer where one CTA owns the SM (0: a single S-MMA warp)
 #define SPION_NSW 0
@@ -1469,7 +1472,7 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     p.off_heavy = rows ? 5 : 6;
     p.off_perm = rows ? 0 : (int)pl.bperm;
     const int grid = ctas * num_sms();
-    int G = (2 * grid + pl.ntiles - 1) / pl.ntiles;
+    int G = (SPION_G_MULT * grid + pl.ntiles - 1) / pl.ntiles;  // (batch, head) per chunk: ~G_MULT items per CTA
     if (G < 1) G = 1;
     if (G > a.bh) G = (int)a.bh;
     p.G = G;
