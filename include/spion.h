@@ -177,7 +177,9 @@ SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, sp
  * dt = SPION_F32: fp32 everywhere on CUDA cores (d <= 128, any block | L).
  * scale: normally 1/sqrt(d) (Eq. 1; reading Q4).
  * Pointers 16-byte aligned; strides in elements, multiples of 8 (bf16) or
- * 4 (fp32).  d <= 128. */
+ * 4 (fp32).  d <= 128.  The CUDA-core path stages one key block in shared
+ * memory: shapes whose staging exceeds 227 KB (e.g. block = 128 with
+ * d = 128) return SPION_ERR_UNSUPPORTED. */
 SPION_API spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, const void *V_dev, void *O_dev,
                             float *lse_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
                             int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,

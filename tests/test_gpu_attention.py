@@ -126,6 +126,8 @@ BF16_CASES = [
     (1024, 64, 64, 2, 0.30, "masked"),
     (1088, 64, 64, 1, 0.25, "paper"),   # nblk = 17 (ragged tile)
     (2048, 32, 64, 2, 0.10, "paper"),   # B=32, nblk = 64
+    (512, 128, 64, 2, 0.5, "paper"),    # B=128: CUDA-core bf16 path (SURVEY 8(b) envelope)
+    (256, 64, 128, 2, 0.5, "masked"),   # d=128: CUDA-core bf16 path
 ]
 
 
@@ -189,8 +191,9 @@ def test_bf16_all_blocks_empty(mode, B):
 
 
 def test_attention_rejects_bad_shapes():
-    """bh = 0 and d beyond the supported head widths are refused with SPION_ERR_SHAPE (raised by
-    the binding), not silently skipped."""
+    """bh = 0 and d beyond the supported head widths are refused with SPION_ERR_SHAPE, and
+    block = 128 with d = 128 (CUDA-core staging beyond 227 KB) with SPION_ERR_UNSUPPORTED
+    (raised by the binding), not silently skipped."""
     spion = _spion()
     from paper_2309_12578_b200 import _native as N
     L, B = 256, 32
@@ -200,6 +203,11 @@ def test_attention_rejects_bad_shapes():
         q = torch.zeros((bh, L, d), dtype=torch.bfloat16, device=DEV)
         with pytest.raises(Exception):
             spion.attn_fwd(q, q, q, bp, "paper", 0.125)
+    bp128 = spion.bsr_from_mask(torch.ones((2, 2), dtype=torch.uint8, device=DEV), 256, 128)
+    q = torch.zeros((1, 256, 128), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(N.SpionError) as ei:
+        spion.attn_fwd(q, q, q, bp128, "paper", 0.125)
+    assert ei.value.status == 7
 
 
 # ------------------------------------------ full BASELINE sizes, sampled slices
