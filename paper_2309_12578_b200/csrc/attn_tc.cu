@@ -89,16 +89,25 @@ __host__ __device__ constexpr int bwd_threads(int mw, int nsw) { return 32 * (mw
 // up to NBUF blocks ahead of the softmax warps; TMA rings have NST >= NBUF stages
 // (which keeps the look-ahead deadlock free).  Two CTAs per SM where they fit (more
 // softmax warps per SM), one CTA with deeper buffering for the B=64 backward.
+#ifndef SPION_DKV_CTAS32
+#define SPION_DKV_CTAS32 2
+#endif
+#ifndef SPION_DKV_NST32
+#define SPION_DKV_NST32 4
+#endif
+#ifndef SPION_FWD_NST32
+#define SPION_FWD_NST32 8
+#endif
 template <int B> struct Cfg {
     static constexpr int FWD_CTAS = 2, FWD_COLS = 256;
     static constexpr int FWD_NBUF = (256 - 64) / B;      // S/P buffers of B columns + O
-    static constexpr int FWD_NST = B == 32 ? 8 : 4;      // K_J + V_J per stage
+    static constexpr int FWD_NST = B == 32 ? SPION_FWD_NST32 : 4;  // K_J + V_J per stage
     static constexpr int DQ_CTAS = B == 32 ? 2 : 1, DQ_COLS = 512 / DQ_CTAS;
     static constexpr int DQ_NBUF = (DQ_COLS - 64) / (2 * B);   // S+dP buffers + dQ
     static constexpr int DQ_NST = B == 32 ? 3 : 8;             // K_J + V_J per stage
-    static constexpr int DKV_CTAS = B == 32 ? 2 : 1, DKV_COLS = 512 / DKV_CTAS;
+    static constexpr int DKV_CTAS = B == 32 ? SPION_DKV_CTAS32 : 1, DKV_COLS = 512 / DKV_CTAS;
     static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
-    static constexpr int DKV_NST = B == 32 ? 4 : 9;               // Q_I + dO_I + lse_I + D_I per stage
+    static constexpr int DKV_NST = B == 32 ? SPION_DKV_NST32 : 9;  // Q_I + dO_I + lse_I + D_I per stage
     // softmax warps of the backward kernels: two warpgroups (each takes half of a block's
     // columns) where one CTA owns the SM, one warpgroup where two CTAs share it
     static constexpr int DQ_MW = DQ_CTAS == 1 ? 8 : 4, DKV_MW = DKV_CTAS == 1 ? 8 : 4;
