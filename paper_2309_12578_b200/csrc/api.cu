@@ -495,7 +495,11 @@ spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, 
                         SPION_SOFTMAX_MASKED, scale, stream);
     if (st) return st;
     if (sumsq_dev) SPION_CUDA_TRY(cudaMemsetAsync(sumsq_dev, 0, sizeof(double), s));
-    return launch_score_mean(Q_dev, K_dev, lse, bh, L, stride_bh, stride_l, scale, A_dev, sumsq_dev, s);
+    // partial tiles of a (batch, head)-split score pass reuse the forward's (dead) O scratch
+    int ks = score_splits(bh, L);
+    while (ks > 1 && (size_t)ks * L * L * 4 > (size_t)bh * L * 64 * 2) --ks;
+    return launch_score_mean(Q_dev, K_dev, lse, bh, L, stride_bh, stride_l, scale, A_dev, sumsq_dev,
+                             reinterpret_cast<float *>(base + o_O), ks, s);
 }
 
 // ------------------------------------------------------------------ NEXT-4: sparse-MHA sub-layer

@@ -36,7 +36,9 @@ bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_
 
 // NEXT-1 dense-phase score mean; scores.cu
 spion_status launch_score_mean(const void *Q, const void *K, const float *lse, int64_t bh, int L, int64_t stride_bh,
-                               int64_t stride_l, float scale, float *A, double *sumsq, cudaStream_t s);
+                               int64_t stride_l, float scale, float *A, double *sumsq, float *part, int ks,
+                               cudaStream_t s);
+int score_splits(int64_t bh, int L);
 
 // NEXT-4 sub-layer kernels; mha.cu
 spion_status launch_heads_permute(const void *src, void *dst, int64_t batch, int L, int W, int H, int d, int to_heads,

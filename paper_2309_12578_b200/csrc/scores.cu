@@ -24,8 +24,8 @@ static constexpr uint32_t SM_TILE = 16384;  // 128 rows x 64 bf16, SW128
 
 __global__ void __launch_bounds__(SM_THREADS, 1)
 score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const float *__restrict__ lse, int64_t bh, int L, float scale_log2, float *__restrict__ A,
-                     double *sumsq) {
+                     const float *__restrict__ lse, int64_t bh_total, int L, float scale_log2, float *__restrict__ out,
+                     double *sumsq, float out_scale) {
     constexpr uint32_t IDESC = idesc_bf16(128, 128, false, false);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -35,6 +35,9 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(s_free + SM_NBUF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
+    // (batch, head) range of this CTA: gridDim.z CTAs split the slices of one tile (partial sums)
+    const int64_t b_lo = bh_total * blockIdx.z / gridDim.z, bh = bh_total * (blockIdx.z + 1) / gridDim.z - b_lo;
+    float *A = out + (int64_t)blockIdx.z * L * L;
     if (threadIdx.x == 0) {
         for (int i = 0; i < SM_NST; ++i) { mbar_init(st_full + i, 1); mbar_init(st_empty + i, 1); }
         for (int i = 0; i < SM_NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(s_free + i, 256); }
@@ -54,8 +57,8 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             mbar_wait(st_empty + st, (u & 1) ^ 1);
             if (elect_one()) {
                 mbar_arrive_expect_tx(st_full + st, 2 * SM_TILE);
-                tma_load_3d(sQ + st * SM_TILE, &tmQ, st_full + st, 0, i0, (int)b);
-                tma_load_3d(sK + st * SM_TILE, &tmK, st_full + st, 0, j0, (int)b);
+                tma_load_3d(sQ + st * SM_TILE, &tmQ, st_full + st, 0, i0, (int)(b_lo + b));
+                tma_load_3d(sK + st * SM_TILE, &tmK, st_full + st, 0, j0, (int)(b_lo + b));
             }
             __syncwarp();
         }
@@ -81,7 +84,7 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         // [0, 64) of every S tile, warps 6-9 columns [64, 128)
         const int r = (warp & 3) * 32 + lane, cg = (warp - 2) >> 2;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16) + cg * 64;
-        const float *lrow = lse + i0 + r;
+        const float *lrow = lse + b_lo * L + i0 + r;
         float acc[64];
 #pragma unroll
         for (int c = 0; c < 64; ++c) acc[c] = 0.f;
@@ -104,7 +107,7 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 acc[32 + c] += ex2(fmaf(v1[c], scale_log2, cur));
             }
         }
-        const float inv = 1.f / (float)bh;
+        const float inv = out_scale;
         float ss = 0.f;
         float4 *dst = reinterpret_cast<float4 *>(A + (int64_t)(i0 + r) * L + j0 + cg * 64);
 #pragma unroll
@@ -127,8 +130,45 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     }
 }
 
+// sum of the gridDim-split partial tiles in slice order (deterministic), scaled; sum of squares
+__global__ void score_reduce_kernel(const float4 *__restrict__ part, int ks, int64_t n4, float inv, float4 *__restrict__ A,
+                                    double *sumsq) {
+    double ss = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 a = __ldg(part + i);
+        for (int z = 1; z < ks; ++z) {
+            const float4 b = __ldg(part + z * n4 + i);
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        a.x *= inv; a.y *= inv; a.z *= inv; a.w *= inv;
+        A[i] = a;
+        ss += (double)(a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w);
+    }
+    if (sumsq) {
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(sumsq, ss);
+    }
+}
+
+// (batch, head) split of each output tile: the one with the best wave efficiency over one CTA
+// per SM (the kernel holds all 512 TMEM columns), the smallest on ties; 1 when the tiles alone
+// fill the GPU (Text: 1024 tiles), e.g. 2 at L = 1024 (64 tiles)
+int score_splits(int64_t bh, int L) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = (int64_t)(L / 128) * (L / 128);
+    int best = 1;
+    double be = -1.0;
+    for (int k = 1; k <= 8 && k <= bh; ++k) {
+        const double w = (double)(tiles * k) / sms, e = w / ceil(w);
+        if (e > be + 1e-9) { be = e; best = k; }
+    }
+    return best;
+}
+
 spion_status launch_score_mean(const void *Q, const void *K, const float *lse, int64_t bh, int L, int64_t stride_bh,
-                               int64_t stride_l, float scale, float *A, double *sumsq, cudaStream_t s) {
+                               int64_t stride_l, float scale, float *A, double *sumsq, float *part, int ks,
+                               cudaStream_t s) {
     alignas(128) CUtensorMap mq, mk;
     if (!tc_make_map(&mq, Q, L, bh, stride_bh, stride_l, 128) || !tc_make_map(&mk, K, L, bh, stride_bh, stride_l, 128))
         return SPION_ERR_CUDA;
@@ -138,9 +178,18 @@ spion_status launch_score_mean(const void *Q, const void *K, const float *lse, i
         SPION_CUDA_TRY(cudaFuncSetAttribute(score_mean_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    score_mean_tc_kernel<<<dim3(L / 128, L / 128), SM_THREADS, smem, s>>>(mq, mk, lse, bh, L, scale * 1.4426950408889634f,
-                                                                         A, sumsq);
+    if (ks < 1 || !part) ks = 1;
+    const float inv = 1.f / (float)bh;
+    score_mean_tc_kernel<<<dim3(L / 128, L / 128, ks), SM_THREADS, smem, s>>>(
+        mq, mk, lse, bh, L, scale * 1.4426950408889634f, ks == 1 ? A : part, ks == 1 ? sumsq : nullptr,
+        ks == 1 ? inv : 1.f);
     SPION_LAUNCH_CHECK();
+    if (ks > 1) {
+        const int64_t n4 = (int64_t)L * L / 4;
+        score_reduce_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float4 *>(part), ks, n4, inv,
+                                                   reinterpret_cast<float4 *>(A), sumsq);
+        SPION_LAUNCH_CHECK();
+    }
     return SPION_OK;
 }
 

@@ -341,7 +341,7 @@ def test_backward_deterministic():
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("bh,L", [(6, 256), (16, 1024), (3, 2048)])
+@pytest.mark.parametrize("bh,L", [(6, 256), (16, 1024), (3, 2048), (64, 1024), (40, 512)])  # last two: (batch, head)-split tiles
 def test_score_mean_matches_oracle(bh, L):
     """NEXT-1: the dense-phase score matrix A^s (mean over (batch, head) of softmax(scale Q K^T))
     and its squared Frobenius norm against the fp64 oracle; rows of A^s sum to 1."""
