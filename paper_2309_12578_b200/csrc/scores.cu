@@ -7,8 +7,8 @@
 // every 128 x 128 output tile once, looping over all bh inside the CTA (no atomics on A):
 //   S = Q_tile K_tile^T (tcgen05, N = 128, into one of 4 TMEM buffers) -> p = 2^(s*scale*log2e
 //   - lse*log2e) accumulated in registers -> A tile = sum / bh, one coalesced store per row.
-// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..9 accumulators (thread = TMEM lane =
-// row; warps 2-5 take columns [0, 64) of every S tile, warps 6-9 columns [64, 128)).
+// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..(AW+1) accumulators (thread = TMEM
+// lane = row; the AW/4 warps of a lane quarter split every S tile's 128 columns).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -19,7 +19,11 @@ namespace spion {
 
 using namespace tc;
 
-static constexpr int SM_NST = 3, SM_NBUF = 4, SM_THREADS = 320;
+#ifndef SPION_SCORE_AW  // accumulator warps (8: 64 columns each, 16: 32 columns each)
+#define SPION_SCORE_AW 16
+#endif
+static constexpr int SM_AW = SPION_SCORE_AW, SM_CPW = 512 / SM_AW;  // columns per accumulator thread
+static constexpr int SM_NST = 3, SM_NBUF = 4, SM_THREADS = 32 * (2 + SM_AW);
 static constexpr uint32_t SM_TILE = 16384;  // 128 rows x 64 bf16, SW128
 
 __global__ void __launch_bounds__(SM_THREADS, 1)
@@ -40,7 +44,7 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     float *A = out + (int64_t)blockIdx.z * L * L;
     if (threadIdx.x == 0) {
         for (int i = 0; i < SM_NST; ++i) { mbar_init(st_full + i, 1); mbar_init(st_empty + i, 1); }
-        for (int i = 0; i < SM_NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(s_free + i, 256); }
+        for (int i = 0; i < SM_NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(s_free + i, 32 * SM_AW); }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -80,14 +84,14 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             __syncwarp();
         }
     } else {
-        // a warp reaches TMEM lanes 32 * (warp % 4) .. + 31: row r = that lane; warps 2-5 take columns
-        // [0, 64) of every S tile, warps 6-9 columns [64, 128)
+        // a warp reaches TMEM lanes 32 * (warp % 4) .. + 31: row r = that lane; the AW / 4 warps of
+        // a lane quarter split the 128 columns of every S tile (SM_CPW each)
         const int r = (warp & 3) * 32 + lane, cg = (warp - 2) >> 2;
-        const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16) + cg * 64;
+        const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16) + cg * SM_CPW;
         const float *lrow = lse + b_lo * L + i0 + r;
-        float acc[64];
+        float acc[SM_CPW];
 #pragma unroll
-        for (int c = 0; c < 64; ++c) acc[c] = 0.f;
+        for (int c = 0; c < SM_CPW; ++c) acc[c] = 0.f;
         float nl2 = bh > 0 ? -lrow[0] * 1.4426950408889634f : 0.f;  // -lse * log2(e), one (batch, head) ahead
         for (int64_t b = 0; b < bh; ++b) {
             const int sb = (int)(b % SM_NBUF);
@@ -95,23 +99,20 @@ score_mean_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             if (b + 1 < bh) nl2 = -lrow[(b + 1) * L] * 1.4426950408889634f;
             mbar_wait(s_full + sb, (uint32_t)(b / SM_NBUF) & 1);
             tc_fence_after();
-            float v0[32], v1[32];
-            tmem_ld32(tl + sb * 128, v0);
-            tmem_ld32(tl + sb * 128 + 32, v1);
+            float v[SM_CPW];
+#pragma unroll
+            for (int h = 0; h < SM_CPW / 32; ++h) tmem_ld32(tl + sb * 128 + 32 * h, *reinterpret_cast<float(*)[32]>(v + 32 * h));
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(s_free + sb);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                acc[c] += ex2(fmaf(v0[c], scale_log2, cur));
-                acc[32 + c] += ex2(fmaf(v1[c], scale_log2, cur));
-            }
+            for (int c = 0; c < SM_CPW; ++c) acc[c] += ex2(fmaf(v[c], scale_log2, cur));
         }
         const float inv = out_scale;
         float ss = 0.f;
-        float4 *dst = reinterpret_cast<float4 *>(A + (int64_t)(i0 + r) * L + j0 + cg * 64);
+        float4 *dst = reinterpret_cast<float4 *>(A + (int64_t)(i0 + r) * L + j0 + cg * SM_CPW);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < SM_CPW / 4; ++c) {
             const float4 q = make_float4(acc[4 * c] * inv, acc[4 * c + 1] * inv, acc[4 * c + 2] * inv, acc[4 * c + 3] * inv);
             ss = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, fmaf(q.w, q.w, ss))));
             dst[c] = q;
