@@ -136,7 +136,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
 }
 // element i of an unrolled row loop: SPION_POLY of every 16 on the FMA pipe, the rest on the SFU
-__device__ __forceinline__ float ex2m(float x, int i) { return (i & 15) < SPION_POLY ? ex2_poly(x) : ex2(x); }  // max entries of one tile list (nblk <= 128)
+__device__ __forceinline__ float ex2m(float x, int i) { return (i & 15) < SPION_POLY ? ex2_poly(x) : ex2(x); }
 static constexpr float LOG2E = 1.4426950408889634f;
 static constexpr float LN2 = 0.6931471805599453f;
 
