@@ -29,6 +29,9 @@ namespace spion {
 #define SPION_HEAVY_FIRST 1
 #endif
 // ---------------------------------------------------------------- K1
+#ifndef SPION_K1_MIN_ROWS  // source rows per warp at least (row split of a block row over CTAs)
+#define SPION_K1_MIN_ROWS 4
+#endif
 #ifndef SPION_K1_PER_SM  // resident K1 CTAs per SM (register cap of the K4 = 4 instantiation)
 #define SPION_K1_PER_SM 3
 #endif
@@ -55,7 +58,7 @@ static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
     const int n_cc = (n + jmax - 1) / jmax;
     g.JC = (n + n_cc - 1) / n_cc;
     g.n_cc = (n + g.JC - 1) / g.JC;
-    // split the rows of a block row over rs CTAs (>= 2 rows per warp each): the rs with the best
+    // split the rows of a block row over rs CTAs (>= K1_MIN_ROWS rows per warp each): the rs with the best
     // wave efficiency (waves / ceil(waves)) over the resident CTA slots, the smallest on ties
     static int slots = 0;
     if (!slots) {
@@ -65,7 +68,7 @@ static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
     }
     int rs = 1;
     double best = -1.0;
-    for (int r = 1; r == 1 || B / (2 * r) >= 2 * K1_WARPS; r *= 2) {
+    for (int r = 1; r == 1 || B / r >= SPION_K1_MIN_ROWS * K1_WARPS; r *= 2) {
         const double w = (double)g.n_cc * n * r / slots, eff = w / ceil(w);
         if (eff > best + 1e-9) { best = eff; rs = r; }
     }
