@@ -449,7 +449,39 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
     for (int r = tid; r < 2 * n; r += nthr)
         sc.cnt[r] = b_popc(b_load(r < n ? sc.flw + r * 4 : sc.colw + (r - n) * 4));
     __syncthreads();
-    if (tid < 32) scan2(sc.cnt, sc.off, n);
+    if (tid < 32) {
+        scan2(sc.cnt, sc.off, n);
+    } else if (a.plan) {
+        // column-tile order (plan bperm), alongside warp 0's scan: block columns by descending
+        // count (stable).  Tiling consecutive columns pairs each stripe column (vertical stripes:
+        // long, overlapping row sets) with band columns, so most of the stripe's union entries
+        // carry one useful slot of S; sorted by count, stripes share tiles with stripes and the
+        // band columns stay mostly consecutive (union entries over the LRA-shaped patterns:
+        // -28 % at Text and Image).  Row tiles keep the natural order.  plan[7]: heavy columns
+        // (more than twice the mean count), a prefix of the order.
+        const PlanLayout pl(n, a.block);
+        const int w = (tid >> 5) - 1, nw = (nthr >> 5) - 1, lane = tid & 31;
+        for (int c = w; c < n; c += nw) {
+            const int cc = SPION_GROUP_HEAVY ? sc.cnt[n + c] : 0;
+            int rank = 0;
+            for (int v0 = 0; v0 < n; v0 += 32) {
+                const int v = v0 + lane;
+                const int cv = v < n ? (SPION_GROUP_HEAVY ? sc.cnt[n + v] : 0) : -1;
+                rank += __popc(__ballot_sync(0xffffffffu, v < n && (cv > cc || (cv == cc && v < c))));
+            }
+            if (lane == 0) sc.perm[rank] = c;
+        }
+        if (w == 0) {
+            int tot = 0;
+            for (int c = lane; c < n; c += 32) tot += sc.cnt[n + c];
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            int hv = 0;
+            for (int c = lane; c < n; c += 32) hv += (long long)sc.cnt[n + c] * n > 2LL * tot;
+            for (int o = 16; o > 0; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
+            if (lane == 0) a.plan[7] = hv;
+            for (int i = n + lane; i < pl.ntiles * pl.S; i += 32) sc.perm[i] = n;
+        }
+    }
     __syncthreads();
     const int nnzb = sc.off[n];
     if (tid == 0) {
@@ -485,31 +517,6 @@ __device__ void build_bsr_and_plan(const K2Args &a, const K2Scratch &sc) {
     int *plan = a.plan;
     __syncthreads();
     k2_stamp(a, 10);
-    // column-tile order: block columns by descending count (stable).  Tiling consecutive columns
-    // pairs each stripe column (vertical stripes: long, overlapping row sets) with band columns,
-    // so most of the stripe's union entries carry one useful slot of S; sorted by count, stripes
-    // share tiles with stripes and the band columns stay mostly consecutive (union entries over
-    // the LRA-shaped patterns: -28 % at Text, -28 % at Image).  Row tiles keep the natural order.
-    // plan[7]: heavy columns (more than twice the mean count), a prefix of the order.
-    for (int c = tid >> 5; c < n; c += nthr >> 5) {
-        const int lane = tid & 31, cc = SPION_GROUP_HEAVY ? sc.cnt[n + c] : 0;
-        int rank = 0;
-        for (int v0 = 0; v0 < n; v0 += 32) {
-            const int v = v0 + lane;
-            const int cv = v < n ? (SPION_GROUP_HEAVY ? sc.cnt[n + v] : 0) : -1;
-            rank += __popc(__ballot_sync(0xffffffffu, v < n && (cv > cc || (cv == cc && v < c))));
-        }
-        if (lane == 0) sc.perm[rank] = c;
-    }
-    if (tid < 32) {
-        const long long nnzb = sc.off[n];
-        int hv = 0;
-        for (int c = tid; c < n; c += 32) hv += (long long)sc.cnt[n + c] * n > 2 * nnzb;
-        for (int o = 16; o > 0; o >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, o);
-        if (tid == 0) plan[7] = hv;
-        for (int i = n + tid; i < pl.ntiles * pl.S; i += 32) sc.perm[i] = n;
-    }
-    __syncthreads();
     for (int i = tid; i < pl.ntiles * pl.S; i += nthr) plan[pl.bperm + i] = sc.perm[i];
     for (int t = tid; t < 2 * pl.ntiles; t += nthr) {
         const bool fwd = t < pl.ntiles;
