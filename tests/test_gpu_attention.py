@@ -112,6 +112,21 @@ def test_fp32_strided_layout():
     _compare(outs, q, k, v, do, fl, B, "paper", 0.2, range(H), 1e-4)
 
 
+def test_bf16_strided_layout():
+    """bf16 [L][heads][d] storage (stride_l = heads*d != d: the CUDA-core path) against the oracle."""
+    spion = _spion()
+    L, B, d, H = 512, 64, 64, 3
+    fl = synth.syn_mask(L // B, 0.3, seed=6)
+    bp = spion.bsr_from_mask(torch.from_numpy(fl).to(DEV), L, B)
+    q, k, v, do = synth.qkvdo(H, L, d, seed=78, dtype=torch.bfloat16)
+    to_strided = lambda x: x.to(DEV).permute(1, 0, 2).contiguous().permute(1, 0, 2)
+    qd, kd, vd, dod = (to_strided(x) for x in (q, k, v, do))
+    o, lse = spion.attn_fwd(qd, kd, vd, bp, "paper", 0.125)
+    dq, dk, dv = spion.attn_bwd(qd, kd, vd, o, dod, lse, bp, "paper", 0.125)
+    outs = [x.float().cpu().numpy() for x in (o, lse, dq, dk, dv)]
+    _compare(outs, q, k, v, do, fl, B, "paper", 0.125, range(H), 2e-2, norm_tol=1e-2, lse_tol=1e-3)
+
+
 # ---------------------------------------------------------------- bf16
 BF16_CASES = [
     # L, B, d, bh, density, mode   (ragged: nblk not a multiple of the 128-row tile)
@@ -362,7 +377,7 @@ def test_transition_host_logic():
     assert spion.transition(9.0, 6.25, 4.84, 0.25) and not spion.transition(9.0, 6.25, 4.84, 0.15)
 
 
-@pytest.mark.parametrize("cfg", ["image", "text"])
+@pytest.mark.parametrize("cfg", ["image", "listops", "text", "retrieval"])
 def test_full_size_sampled_masked(cfg):
     """The MASKED softmax (rows of P sum to 1, reading Q1) at full BASELINE sizes, sampled slices."""
     spion = _spion()
