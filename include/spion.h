@@ -172,8 +172,8 @@ SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, sp
  * Rows whose block-row is empty: O_i = 0, lse_i = ln L (PAPER) / -inf (MASKED).
  * dt = SPION_BF16: bf16 Q/K/V/O, fp32 accumulation, P rounded to bf16 before
  *   P.V on the tensor-core path (reading Q18).  Tensor-core (tcgen05) path
- *   for block in {32, 64} and d == 64 with stride_l == d; other shapes run
- *   the CUDA-core path.
+ *   for block in {32, 64} and d == 64 (any strides that are multiples of 8
+ *   elements: strided TMA tensor maps); other shapes run the CUDA-core path.
  * dt = SPION_F32: fp32 everywhere on CUDA cores (d <= 128, any block | L).
  * scale: normally 1/sqrt(d) (Eq. 1; reading Q4).
  * Pointers 16-byte aligned; strides in elements, multiples of 8 (bf16) or

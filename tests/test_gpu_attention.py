@@ -113,7 +113,8 @@ def test_fp32_strided_layout():
 
 
 def test_bf16_strided_layout():
-    """bf16 [L][heads][d] storage (stride_l = heads*d != d: the CUDA-core path) against the oracle."""
+    """bf16 [L][heads][d] storage (stride_l = heads*d, stride_bh = d: strided TMA tensor maps on
+    the tensor-core path) against the oracle."""
     spion = _spion()
     L, B, d, H = 512, 64, 64, 3
     fl = synth.syn_mask(L // B, 0.3, seed=6)
