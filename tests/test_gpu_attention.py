@@ -255,11 +255,12 @@ def test_full_size_sampled(cfg):
              lse_tol=1e-3)
 
 
-@pytest.mark.parametrize("bh", [16, 256, 512])
-def test_step_host_matches_device_calls(bh):
+@pytest.mark.parametrize("bh,dtype,mode", [(16, "bf16", "paper"), (256, "bf16", "paper"), (512, "bf16", "masked"),
+                                           (48, "f32", "paper")])
+def test_step_host_matches_device_calls(bh, dtype, mode):
     """spion_step_host (pipelined over (batch, head) chunks, host buffers) gives the same bytes as
-    spion_pattern + spion_attn_fwd + spion_attn_bwd on device buffers (bh = 16 / 256 / 512 run
-    as 1 / 8 / 16 chunks)."""
+    spion_pattern + spion_attn_fwd + spion_attn_bwd on device buffers (bf16 bh = 16 / 256 / 512 run
+    as 1 / 8 / 16 chunks; fp32 on the CUDA-core path)."""
     import ctypes
 
     spion = _spion()
@@ -267,24 +268,26 @@ def test_step_host_matches_device_calls(bh):
 
     L, B, d = 1024, 32, 64
     A = synth.lra_scores(L, B, seed=5)
-    q, k, v, do = synth.qkvdo(bh, L, d, seed=77, dtype=torch.bfloat16)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q, k, v, do = synth.qkvdo(bh, L, d, seed=77, dtype=tdt)
     scale = 1 / math.sqrt(d)
     bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
     qd, kd, vd, dod = (x.to(DEV) for x in (q, k, v, do))
-    o, lse = spion.attn_fwd(qd, kd, vd, bp, "paper", scale)
-    dq, dk, dv = spion.attn_bwd(qd, kd, vd, o, dod, lse, bp, "paper", scale)
+    o, lse = spion.attn_fwd(qd, kd, vd, bp, mode, scale)
+    dq, dk, dv = spion.attn_bwd(qd, kd, vd, o, dod, lse, bp, mode, scale)
     torch.cuda.synchronize()
     lib = N.lib()
     hA = A.pin_memory()
     hq, hk, hv, hdo = (x.pin_memory() for x in (q, k, v, do))
     ho, hdq, hdk, hdv = (torch.empty_like(hq).pin_memory() for _ in range(4))
     hlse = torch.empty((bh, L), dtype=torch.float32).pin_memory()
-    nb = lib.spion_step_arena_bytes(bh, L, d, B, N.BF16)
+    ndt = N.BF16 if dtype == "bf16" else N.F32
+    nb = lib.spion_step_arena_bytes(bh, L, d, B, ndt)
     arena = torch.empty(nb, dtype=torch.uint8, device=DEV)
     P = lambda t: ctypes.c_void_p(t.data_ptr())
     nnz = ctypes.c_int32(0)
     st = lib.spion_step_host(P(hA), P(hq), P(hk), P(hv), P(hdo), P(ho), P(hlse), P(hdq), P(hdk), P(hdv), bh, L, d, B,
-                             31, 75.0, N.THRESH["linear"], N.BF16, N.SOFTMAX["paper"], scale, P(arena), nb,
+                             31, 75.0, N.THRESH["linear"], ndt, N.SOFTMAX[mode], scale, P(arena), nb,
                              ctypes.byref(nnz), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     N.check(st, "spion_step_host")
     assert nnz.value == bp.nnzb
