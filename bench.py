@@ -3,11 +3,15 @@
 synthetic head-averaged score matrix (Alg. 3/4) + block-sparse attention
 forward + backward over every (batch, head) of the LRA-shaped workload.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config image|listops|text|retrieval]
-    torchrun --nproc-per-node N bench.py --gpus N ...          (one rank per GPU, NCCL)
-    python bench.py --impl reference ...                       (the CPU oracle, bounded sample)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config text|image|listops|retrieval]
+    python bench.py --gpus 8 ...          (re-launches itself under torch.distributed.run, one rank per GPU)
+    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...  (the CPU oracle, bounded sample per step)
 
-Prints ONE JSON line on rank 0 (contract in DESIGN.md §6).
+Default workload: LRA Text (BASELINE configs[3], the largest single-GPU config).
+Multi-GPU: strong scaling by default — the config's global (batch x head) slices are
+split into N contiguous shards; `--scaling weak` gives every rank the
+whole config.  Prints ONE JSON line on rank 0 (contract in DESIGN.md section 7).
 """
 from __future__ import annotations
 
@@ -16,6 +20,7 @@ import json
 import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -23,23 +28,27 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
 from paper_2309_12578_b200 import accounting  # noqa: E402
+from paper_2309_12578_b200.dist import shard  # noqa: E402
 
 METRIC = "sparse-attn fwd+bwd tokens/s at LRA shapes; % bf16 tensor peak on useful blocks"
 UNIT = "tokens/s"
 
-# BASELINE.json configs (d = 64, bf16); towers = 2 for Retrieval (two documents)
+# BASELINE.json configs (d = 64, bf16); towers = 2 for Retrieval (two documents).  alpha: the
+# flood-fill quantile that puts the block density of the synthetic LRA scores near the north
+# star's ~10 % (~90 % block sparsity): measured with the oracle on synth.lra_scores seeds 1 / 1001
+# (DESIGN.md section 5): Image 11.8 / 10.7 %, ListOps 12.6 / 9.9 %, Text 10.1 / 10.0 %.
 CONFIGS = {
-    "image": dict(workload="lra_image", L=1024, block=32, heads=4, d=64, batch=64, towers=1),
-    "listops": dict(workload="lra_listops", L=2048, block=64, heads=8, d=64, batch=32, towers=1),
-    "text": dict(workload="lra_text", L=4096, block=64, heads=8, d=64, batch=16, towers=1),
-    "retrieval": dict(workload="lra_retrieval", L=4096, block=64, heads=8, d=64, batch=16, towers=2),
+    "image": dict(workload="lra_image", L=1024, block=32, heads=4, d=64, batch=64, towers=1, alpha=75.0),
+    "listops": dict(workload="lra_listops", L=2048, block=64, heads=8, d=64, batch=32, towers=1, alpha=75.0),
+    "text": dict(workload="lra_text", L=4096, block=64, heads=8, d=64, batch=16, towers=1, alpha=55.0),
+    "retrieval": dict(workload="lra_retrieval", L=4096, block=64, heads=8, d=64, batch=16, towers=2, alpha=55.0),
 }
 FILTER = 31
+SCORE_SEEDS = (1, 1001)  # the score matrices of the rotating input sets (set s uses SCORE_SEEDS[s % 2])
 
 
 def load_peaks():
@@ -52,7 +61,7 @@ def load_peaks():
 
 
 # DRAM bytes per launch of each call from one `ncu --set full` capture (tools/ncu_traffic.py)
-TRAFFIC_FILE = "profiles/r1/ncu_traffic.json"
+TRAFFIC_FILE = "profiles/r2/ncu_traffic.json"
 
 
 def ncu_traffic(config, call):
@@ -62,6 +71,18 @@ def ncu_traffic(config, call):
         return float(v) if v is not None else None
     except (OSError, ValueError):
         return None
+
+
+def config_dict(cfg, args, world):
+    """The workload description both arms print (identical for the same flags)."""
+    bh = cfg["batch"] * cfg["towers"] * cfg["heads"]
+    return {
+        "workload": cfg["workload"], "L": cfg["L"], "block": cfg["block"], "heads": cfg["heads"], "d": cfg["d"],
+        "batch": cfg["batch"], "towers": cfg["towers"], "bh": bh, "filter": FILTER, "alpha": args.alpha,
+        "softmax": args.mode, "step": "pattern(scores)+attn_fwd+attn_bwd",
+        "parallelism": f"dp{world} over batch*head ({args.scaling} scaling)",
+        "l2": "rotating input sets, >= 2x L2 of other data between two uses of a set",
+    }
 
 
 # ------------------------------------------------------------------ clocks
@@ -87,15 +108,20 @@ class ClockSampler:
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.02)
+            self.sample()
+            time.sleep(0.01)
+
+    def sample(self):
+        if not self.nv:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    self.reasons.add(name)
+        except Exception:
+            pass
 
     def __enter__(self):
         if self.nv:
@@ -107,6 +133,7 @@ class ClockSampler:
         self._stop.set()
         if self.nv:
             self.t.join()
+            self.sample()
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
@@ -114,15 +141,33 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed
-def dist_setup(n_gpus: int):
+def maybe_self_launch(args):
+    """`--gpus N` (N > 1) without a torch.distributed environment: re-launch this script under
+    torch.distributed.run with one rank per GPU (rendezvous on 127.0.0.1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
+
+
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group("gloo")
         return dist, rank, world, local
     return None, 0, 1, 0
 
@@ -132,160 +177,280 @@ def barrier(dist):
         dist.barrier()
 
 
+def rank_slices(cfg, scaling, rank, world):
+    """(start, stop) of this rank's global (batch x head) slices."""
+    bh_total = cfg["batch"] * cfg["towers"] * cfg["heads"]
+    if scaling == "weak":
+        return rank * bh_total, (rank + 1) * bh_total
+    return shard(bh_total, rank, world)
+
+
 # ------------------------------------------------------------------ oracle leg
-def oracle_sample(cfg, mask_fl, alpha, budget_s=20.0, seed=99):
-    """Time the CPU oracle (as it stands) on a bounded sample of the step: the pattern once
-    plus fwd+bwd of k (batch, head) slices run concurrently on all host cores; the step time
-    is extrapolated linearly to every (batch, head).  Returns (tokens/s, cores, description)."""
+def oracle_scores(cfg):
+    return synth.lra_scores(cfg["L"], cfg["block"], seed=SCORE_SEEDS[0]).numpy()
+
+
+def oracle_step(cfg, alpha, mode, slices, A, cores, seed=99):
+    """One bounded oracle step: the pattern (Alg. 3/4) once, then fwd+bwd of the given (batch, head)
+    slices, one slice per host thread (the oracle's C calls release the GIL).  Returns
+    (seconds, pattern seconds, blocks)."""
     import concurrent.futures as cf
 
     import oracle
 
     L, B, d = cfg["L"], cfg["block"], cfg["d"]
-    bh = cfg["batch"] * cfg["towers"] * cfg["heads"]
-    tokens = cfg["batch"] * cfg["towers"] * L
-    cores = os.cpu_count() or 1
-    A = synth.lra_scores(L, B, seed=1).numpy()
+    scale = 1.0 / math.sqrt(d)
     t0 = time.perf_counter()
     fl, _, _ = oracle.pattern(A, B, FILTER, alpha)
     t_pat = time.perf_counter() - t0
-    scale = 1.0 / math.sqrt(d)
 
     def one(b):
         q, k, v, do = (x[0].double().numpy() for x in synth.qkvdo(1, L, d, seed=seed, dtype=torch.bfloat16,
                                                                   start_bh=b))
-        t = time.perf_counter()
-        oracle.attn_fwd(q, k, v, fl, B, scale, "paper")
-        oracle.attn_bwd(q, k, v, do, fl, B, scale, "paper")
-        return time.perf_counter() - t
+        oracle.attn_fwd(q, k, v, fl, B, scale, mode)
+        oracle.attn_bwd(q, k, v, do, fl, B, scale, mode)
 
-    # calibrate with one slice, then size the sample to the budget
-    t1 = one(0)
-    k = int(max(1, min(bh - 1, budget_s / max(t1, 1e-6) * cores * 0.8)))
-    k = max(cores, (k // cores) * cores) if k >= cores else k
-    k = min(k, bh - 1) if bh > 1 else 0
-    t0 = time.perf_counter()
-    if k > 0:
+    if slices:
         with cf.ThreadPoolExecutor(max_workers=cores) as ex:
-            list(ex.map(one, range(1, 1 + k)))
-    wall = time.perf_counter() - t0
-    per_slice_parallel = (wall / k) if k > 0 else t1
-    t_step = t_pat + per_slice_parallel * bh
-    desc = (f"pattern once ({t_pat:.2f}s) + fwd+bwd of {k + 1} of {bh} (batch,head) slices "
-            f"({k} concurrently on {cores} threads in {wall:.2f}s); extrapolated linearly to all {bh}")
-    return tokens / t_step, cores, desc, t_step
+            list(ex.map(one, slices))
+    return time.perf_counter() - t0, t_pat, int(fl.sum())
+
+
+def oracle_single_slice_seconds(cfg, alpha, mode, A):
+    """Single-thread seconds of fwd+bwd for one (batch, head) slice."""
+    import oracle
+
+    L, B, d = cfg["L"], cfg["block"], cfg["d"]
+    fl, _, _ = oracle.pattern(A, B, FILTER, alpha)
+    q, k, v, do = (x[0].double().numpy() for x in synth.qkvdo(1, L, d, seed=99, dtype=torch.bfloat16))
+    t = time.perf_counter()
+    oracle.attn_fwd(q, k, v, fl, B, 1.0 / math.sqrt(d), mode)
+    oracle.attn_bwd(q, k, v, do, fl, B, 1.0 / math.sqrt(d), mode)
+    return time.perf_counter() - t
+
+
+def oracle_sample(cfg, alpha, mode, budget_s, bh_total):
+    """cpu_baseline leg (N=1, rank 0): the oracle as it stands on all host cores, on a bounded
+    sample (~budget_s of CPU work): pattern once + fwd+bwd of k slices."""
+    cores = os.cpu_count() or 1
+    A = oracle_scores(cfg)
+    t1 = oracle_single_slice_seconds(cfg, alpha, mode, A)
+    k = int(max(1, min(bh_total, budget_s / max(t1, 1e-6) * cores * 0.8)))
+    if k >= cores:
+        k = (k // cores) * cores
+    secs, t_pat, _ = oracle_step(cfg, alpha, mode, list(range(k)), A, cores)
+    tokens = k * cfg["L"] / cfg["heads"]  # a (batch, head) slice is 1/heads of L tokens' attention work
+    desc = (f"pattern once ({t_pat:.2f}s) + fwd+bwd of {k} of {bh_total} (batch,head) slices on {cores} threads "
+            f"in {secs - t_pat:.2f}s; value = the sample's tokens ({k} slices x L / heads) / its measured time")
+    return {"value": tokens / secs, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+            "single_thread_slice_s": t1, "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, cfg):
-    dist, rank, world, _ = dist_setup(args.gpus)
-    if rank != 0:
+    """--impl reference: the oracle (this tier's reference arm) timed on the host cores, K steps
+    after W warm-up steps; each step = the pattern + fwd+bwd of a bounded sample of (batch, head)
+    slices (sized so the whole run takes ~--cpu-budget-total seconds); value = the sample's tokens
+    over the measured step time.  Under torchrun only rank 0 runs."""
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:  # the oracle runs once, on rank 0's host cores; the other ranks exit without work
         return
-    per_rank_cfg = dict(cfg)
-    value, cores, desc, t_step = oracle_sample(per_rank_cfg, None, args.alpha, budget_s=args.cpu_budget)
+    cores = os.cpu_count() or 1
+    A = oracle_scores(cfg)
+    a, b = rank_slices(cfg, args.scaling, 0, 1)
+    bh_total = (b - a) * (world if args.scaling == "weak" else 1)
+    t1 = oracle_single_slice_seconds(cfg, args.alpha, args.mode, A)
+    per_step_budget = args.cpu_budget_total / (args.steps + args.warmup)
+    k = int(max(1, min(bh_total, per_step_budget / max(t1, 1e-6) * cores * 0.8)))
+    if k >= cores:
+        k = (k // cores) * cores
+    slices = list(range(k))
+    for _ in range(args.warmup):
+        oracle_step(cfg, args.alpha, args.mode, slices, A, cores)
+    times = []
+    for _ in range(args.steps):
+        secs, t_pat, nnzb = oracle_step(cfg, args.alpha, args.mode, slices, A, cores)
+        times.append(secs)
+    t_step = statistics.mean(times)  # measured seconds per (sampled) step, pattern included
+    tokens = k * cfg["L"] / cfg["heads"]  # a (batch, head) slice is 1/heads of L tokens' attention work
+    value = tokens / t_step
+    desc = (f"{args.steps} timed steps after {args.warmup} warm-up; each step = the pattern (Alg. 3/4) once + "
+            f"fwd+bwd of {k} of the config's {bh_total} (batch,head) slices on {cores} threads; value = the "
+            f"sample's tokens ({k} slices x L / heads) / measured step time (no extrapolation)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "L": cfg["L"], "block": cfg["block"], "heads": cfg["heads"],
-                   "d": cfg["d"], "batch": cfg["batch"], "towers": cfg["towers"], "alpha": args.alpha,
-                   "filter": FILTER},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, args, world),
+        "pattern": {"nnzb": nnzb, "score_seed": SCORE_SEEDS[0]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                         "single_thread_slice_s": t1, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU leg
+class Phases:
+    """One step's calls, eager or as three CUDA graphs (pattern / fwd / bwd) with timing events
+    recorded between the graph launches on the launching stream."""
+
+    def __init__(self, fns, use_graphs, stream):
+        self.fns, self.graphs, self.stream = fns, None, stream
+        if use_graphs:
+            self.graphs = []
+            for fn in fns:
+                if fn is None:
+                    self.graphs.append(None)
+                    continue
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    fn()
+                self.graphs.append(g)
+
+    def run(self, k):
+        if self.graphs is not None:
+            g = self.graphs[k]
+            if g is not None:
+                g.replay()
+        elif self.fns[k] is not None:
+            self.fns[k]()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="spion", choices=["spion", "reference"])
-    ap.add_argument("--config", default="image", choices=sorted(CONFIGS))
-    ap.add_argument("--alpha", type=float, default=75.0,
-                    help="flood-fill quantile (75 gives ~9-12%% block density on the synthetic LRA scores)")
+    ap.add_argument("--config", default="text", choices=sorted(CONFIGS))
+    ap.add_argument("--alpha", type=float, default=None,
+                    help="flood-fill quantile (default per config: ~10%% block density on the synthetic scores)")
     ap.add_argument("--mode", default="paper", choices=["paper", "masked"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of CUDA-graph replays")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="cpu_baseline leg: seconds of oracle work")
+    ap.add_argument("--cpu-budget-total", type=float, default=120.0, help="--impl reference: seconds for the run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--phase-detail", action="store_true", help="also print per-phase timings to stderr")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.alpha is None:
+        args.alpha = cfg["alpha"]
     if args.warmup < 3:
         args.warmup = 3
+    if maybe_self_launch(args):
+        return
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     from paper_2309_12578_b200 import spion
     from paper_2309_12578_b200 import _native as N
     from paper_2309_12578_b200.dist import broadcast_pattern
 
-    dist, rank, world, local = dist_setup(args.gpus)
+    dist, rank, world, local = dist_setup()
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     hbm_peak, tc_peak, tc_sust, peak_src = load_peaks()
 
     L, B, H, d = cfg["L"], cfg["block"], cfg["heads"], cfg["d"]
-    bh = cfg["batch"] * cfg["towers"] * H          # per rank (weak scaling over ranks)
-    tokens_rank = cfg["batch"] * cfg["towers"] * L
+    s0, s1 = rank_slices(cfg, args.scaling, rank, world)
+    bh = s1 - s0                                         # this rank's (batch, head) slices
+    bh_total = cfg["batch"] * cfg["towers"] * H * (world if args.scaling == "weak" else 1)
+    tokens_job = bh_total // H * L                       # tokens of the whole job per step
     scale = 1.0 / math.sqrt(d)
 
-    # inputs resident in HBM; two rotating sets so a step never finds its inputs in L2
-    NSETS = 2
-    sets = []
+    # inputs resident in HBM; rotating sets so that between two uses of a set at least 2x the L2
+    # of other data is touched (a step never finds its inputs in L2)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    set_bytes = 4 * L * L + 9 * bh * L * d * 2 + 2 * bh * L * 4
+    NSETS = max(2, min(16, math.ceil(2 * l2 / set_bytes) + 1))
+    scores_cpu = [synth.lra_scores(L, B, seed=sd) for sd in SCORE_SEEDS]
+    sets, outs = [], []
     for s in range(NSETS):
-        A = synth.lra_scores(L, B, seed=1 + 1000 * s, device=dev)
-        q, k, v, do = synth.qkvdo(bh, L, d, seed=7 + 100003 * s, dtype=torch.bfloat16, device=dev,
-                                  start_bh=rank * bh)
+        A = scores_cpu[s % 2].to(dev)
+        q, k, v, do = synth.qkvdo(bh, L, d, seed=7 + 100003 * s, dtype=torch.bfloat16, device=dev, start_bh=s0)
         sets.append((A, q, k, v, do))
-    outs = [dict(o=torch.empty_like(q), lse=torch.empty((bh, L), dtype=torch.float32, device=dev),
-                 dq=torch.empty_like(q), dk=torch.empty_like(q), dv=torch.empty_like(q)) for _ in range(NSETS)]
-    ws = spion.attn_workspace(bh, L, d, torch.bfloat16, dev)
+        outs.append(dict(o=torch.empty_like(q), lse=torch.empty((bh, L), dtype=torch.float32, device=dev),
+                         dq=torch.empty_like(q), dk=torch.empty_like(q), dv=torch.empty_like(q),
+                         ws=spion.attn_workspace(bh, L, d, torch.bfloat16, dev)))
     bps = [spion.empty_pattern(L, B, dev) for _ in range(NSETS)]
-    # (pattern workspace is attached to each BlockPattern on first use)
+    stream = torch.cuda.Stream(dev)
 
-    def step(i, ev=None):
-        A, q, k, v, do = sets[i % NSETS]
-        o = outs[i % NSETS]
-        bp = bps[i % NSETS]
-        if ev is not None:
-            ev[0].record()
-        if rank == 0 or world == 1:
-            spion.pattern(A, B, filter=FILTER, alpha=args.alpha, out=bp)
+    def make_phases(i):
+        A, q, k, v, do = sets[i]
+        o, bp = outs[i], bps[i]
+        pat = (lambda: spion.pattern(A, B, filter=FILTER, alpha=args.alpha, out=bp)) if (rank == 0 or world == 1) \
+            else None
+        fwd = lambda: spion.attn_fwd(q, k, v, bp, args.mode, scale, out=o["o"], lse=o["lse"], workspace=o["ws"])
+        bwd = lambda: spion.attn_bwd(q, k, v, o["o"], do, o["lse"], bp, args.mode, scale, workspace=o["ws"],
+                                     dq=o["dq"], dk=o["dk"], dv=o["dv"])
+        return [pat, fwd, bwd]
+
+    with torch.cuda.stream(stream):
+        # eager pass first: allocates every pattern workspace, fills the descriptor caches, and
+        # counts this library's kernel launches per step
+        l0 = spion.launch_count()
+        for i in range(NSETS):
+            for fn in make_phases(i):
+                if fn is not None:
+                    fn()
         if world > 1:
-            broadcast_pattern(bp.flat, src=0)  # the per-layer pattern: one NCCL collective
-        if ev is not None:
-            ev[1].record()
-        spion.attn_fwd(q, k, v, bp, args.mode, scale, out=o["o"], lse=o["lse"])
-        if ev is not None:
-            ev[2].record()
-        spion.attn_bwd(q, k, v, o["o"], do, o["lse"], bp, args.mode, scale, workspace=ws,
-                       dq=o["dq"], dk=o["dk"], dv=o["dv"])
-        if ev is not None:
-            ev[3].record()
+            for bp in bps:
+                broadcast_pattern(bp.flat, src=0)
+        launches_per_step = (spion.launch_count() - l0) / NSETS
+        torch.cuda.synchronize()
+        phases = [Phases(make_phases(i), not args.no_graphs, stream) for i in range(NSETS)]
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    nnzb_sets = [bp_.nnzb for bp_ in bps]  # steps alternate between the sets' patterns
+        def step(i, ev=None):
+            j = i % NSETS
+            ph = phases[j]
+            if ev is not None:
+                ev[0].record(stream)
+            ph.run(0)
+            if world > 1:
+                broadcast_pattern(bps[j].flat, src=0)  # the per-layer pattern: one NCCL collective
+            if ev is not None:
+                ev[1].record(stream)
+            ph.run(1)
+            if ev is not None:
+                ev[2].record(stream)
+            ph.run(2)
+            if ev is not None:
+                ev[3].record(stream)
+
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+    nnzb_sets = [bp_.nnzb for bp_ in bps[:2]]
     nnzb = sum(nnzb_sets) / len(nnzb_sets)
     density = nnzb / (L // B) ** 2
 
-    # ---- timed region: K steps, events on the launching stream at phase boundaries
+    # ---- timed region: K steps; events on the launching stream at the phase boundaries
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = spion.launch_count()
-    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+    with torch.cuda.stream(stream), ClockSampler(dev.index if dev.index is not None else 0) as clk:
         barrier(dist)
         torch.cuda.synchronize()
-        start.record()
+        start.record(stream)
         for i in range(args.steps):
             step(i, evs[i])
-        end.record()
+        end.record(stream)
         torch.cuda.synchronize()
         barrier(dist)
-    launches = spion.launch_count() - launches0
+    launches = int(round(launches_per_step * args.steps))
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -307,33 +472,34 @@ def main():
     }
     flops = {"pattern": 0, "fwd": accounting.useful_flops(B, d, nnzb, bh, True, False),
              "bwd": accounting.useful_flops(B, d, nnzb, bh, False, True)}
-    dom = max(ph_ms, key=ph_ms.get)
+    dom = max(("fwd", "bwd"), key=ph_ms.get)
     t_dom = ph_ms[dom] * 1e-3
     gbs = alg[dom] / t_dom / 1e9
-    traffic = ncu_traffic(args.config, dom)
-    roofline = {"kernel": f"spion_attn_{dom}" if dom != "pattern" else "spion_pattern", "bound": "hbm",
+    traffic = ncu_traffic(args.config, dom) if world == 1 else None
+    roofline = {"kernel": f"spion_attn_{dom}", "bound": "hbm",
                 "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "traffic": traffic,
                 "traffic_source": TRAFFIC_FILE if traffic is not None else None,
-                "peak_source": peak_src, "alg_bytes_per_launch": alg[dom], "ms_per_launch": ph_ms[dom],
-                "useful_tflops": flops[dom] / t_dom / 1e12 if flops[dom] else 0.0}
+                "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs: copy bandwidth)",
+                "alg_bytes_per_launch": alg[dom], "alg_bytes_per_row": (16 * d + 4) if dom == "bwd" else (8 * d + 4),
+                "ms_per_launch": ph_ms[dom], "useful_tflops": flops[dom] / t_dom / 1e12 if flops[dom] else 0.0}
     step_flops = accounting.useful_flops(B, d, nnzb, bh)
-    value = tokens_rank * world / (ms * 1e-3)
+    value = tokens_job / (ms * 1e-3)
 
-    # ---- end to end through the C ABI from pinned host buffers (H2D + D2H inside)
+    # ---- end to end through the C ABI from pinned host buffers (H2D + D2H inside the timed region)
     e2e = None
     if args.e2e_steps > 0:
+        import ctypes
         lib = N.lib()
         A, q, k, v, do = sets[0]
-        hA = A.cpu().pin_memory()
+        hA = scores_cpu[0].pin_memory()
         hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
         ho, hdq, hdk, hdv = (torch.empty_like(hq).pin_memory() for _ in range(4))
         hlse = torch.empty((bh, L), dtype=torch.float32).pin_memory()
         arena_bytes = lib.spion_step_arena_bytes(bh, L, d, B, N.BF16)
         arena = torch.empty(arena_bytes, dtype=torch.uint8, device=dev)
-        import ctypes
         P = lambda t: ctypes.c_void_p(t.data_ptr())
         nnz = ctypes.c_int32(0)
-        strm = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        strm = ctypes.c_void_p(stream.cuda_stream)
 
         def host_step():
             st = lib.spion_step_host(P(hA), P(hq), P(hk), P(hv), P(hdo), P(ho), P(hlse), P(hdq), P(hdk), P(hdv),
@@ -344,10 +510,10 @@ def main():
         host_step()
         barrier(dist)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(stream)
         for _ in range(args.e2e_steps):
             host_step()
-        e1.record()
+        e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / args.e2e_steps
         if world > 1:
@@ -355,29 +521,26 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         tb = bh * L * d * 2
-        e2e = {"value": tokens_rank * world / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": L * L * 4 + 4 * tb,
-               "d2h_bytes_per_step": 4 * tb + bh * L * 4, "ms_per_step": ems}
+        e2e = {"value": tokens_job / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": L * L * 4 + 4 * tb,
+               "d2h_bytes_per_step": 4 * tb + bh * L * 4, "ms_per_step": ems,
+               "path": "spion_step_host (pinned host buffers, per rank)"}
         del arena
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v_, cores, desc, _ = oracle_sample(cfg, None, args.alpha, budget_s=args.cpu_budget)
-        cpu = {"value": v_, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = oracle_sample(cfg, args.alpha, args.mode, args.cpu_budget, bh)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {
-                "workload": cfg["workload"], "L": L, "block": B, "heads": H, "d": d, "batch_per_rank": cfg["batch"],
-                "towers": cfg["towers"], "bh_per_rank": bh, "filter": FILTER, "alpha": args.alpha,
-                "softmax": args.mode, "nnzb": nnzb, "nnzb_sets": nnzb_sets, "block_density": round(density, 4),
-                "step": "pattern(scores)+attn_fwd+attn_bwd", "parallelism": f"dp{world} over batch*head",
-                "l2": f"{NSETS} rotating input sets (> L2 per step)",
-            },
+            "config": config_dict(cfg, args, world),
+            "pattern": {"nnzb": nnzb, "nnzb_sets": nnzb_sets, "block_density": round(density, 4),
+                        "score_seeds": list(SCORE_SEEDS)},
+            "bh_per_rank": bh, "input_sets": NSETS, "cuda_graphs": not args.no_graphs,
             "phases_ms": ph_ms,
-            "useful_tflops": step_flops / (ms * 1e-3) / 1e12 * world,
+            "useful_tflops": step_flops * world / (ms * 1e-3) / 1e12,
             "pct_bf16_peak_useful": 100.0 * step_flops * world / (ms * 1e-3) / (tc_peak * 1e12 * world),
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -157,11 +157,29 @@ SPION_API spion_status spion_pattern_check(const void *ws_dev, int32_t *flags_ho
 SPION_API spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t block, spion_bsr *out,
                                  int32_t *nnzb_host, void *stream);
 
-/* Bytes of device workspace spion_attn_bwd needs: D_i = rowsum(dO*O), fp32
- * [bh][L], and -lse_i*log2(e), fp32 [bh][L] (written by the dQ pass for the
- * dK/dV pass; the backward is atomic-free and deterministic).  spion_attn_fwd
- * needs none. */
+/* Attention workspaces (device, caller-owned, 16-byte aligned).  The first 256
+ * bytes hold the tensor-core kernels' work-item counters; every call zeroes
+ * them (one cudaMemsetAsync on `stream`) before launching, so calls that
+ * share one pattern may run concurrently on different streams as long as
+ * each has its OWN workspace.  A workspace must not be shared by calls that
+ * can run concurrently.
+ * spion_attn_fwd_workspace_bytes: the counters only (256 bytes).
+ * spion_attn_workspace_bytes: the counters, then D_i = rowsum(dO*O) and
+ * -lse_i*log2(e), fp32 [bh][L] each (written by the dQ pass for the dK/dV
+ * pass; the backward is atomic-free and deterministic).  Enough for either
+ * call. */
+SPION_API size_t spion_attn_fwd_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt);
 SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt);
+
+/* Which kernels spion_attn_fwd / spion_attn_bwd run for these arguments
+ * (host only, nothing is launched): SPION_PATH_TCGEN05 — the tensor-core
+ * kernels (bf16, d == 64, block in {32, 64}, strides multiples of 8, L % 4 ==
+ * 0, nblk <= 128, plan present, driver entry point cuTensorMapEncodeTiled
+ * available, SPION_DISABLE_TC unset); SPION_PATH_CUDA_CORE — the CUDA-core
+ * kernels; a negative value -status if the call would be rejected. */
+typedef enum { SPION_PATH_CUDA_CORE = 0, SPION_PATH_TCGEN05 = 1 } spion_attn_path_kind;
+SPION_API int32_t spion_attn_path(int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l,
+                                  spion_dtype dt, const spion_bsr *pat);
 
 /* Forward block-sparse attention, per (batch, head) b (Alg. 5 l.4-8,
  * P:662-670; Eq. 5; Alg. 6):
@@ -179,11 +197,12 @@ SPION_API size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, sp
  * Pointers 16-byte aligned; strides in elements, multiples of 8 (bf16) or
  * 4 (fp32).  d <= 128.  The CUDA-core path stages one key block in shared
  * memory: shapes whose staging exceeds 227 KB (e.g. block = 128 with
- * d = 128) return SPION_ERR_UNSUPPORTED. */
+ * d = 128) return SPION_ERR_UNSUPPORTED.
+ * ws_dev: >= spion_attn_fwd_workspace_bytes(...) bytes (see above). */
 SPION_API spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, const void *V_dev, void *O_dev,
                             float *lse_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
                             int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,
-                            float scale, void *stream);
+                            float scale, void *ws_dev, size_t ws_bytes, void *stream);
 
 /* Backward of spion_attn_fwd (the paper's custom autograd; formulas
  * of reading Q17): with p_ij = exp(s_ij - lse_i) and D_i = dO_i . O_i,
@@ -191,7 +210,8 @@ SPION_API spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, cons
  *   dQ_i = scale sum_j ds_ij K_j ; dK_j = scale sum_i ds_ij Q_i ; dV_j = sum_i p_ij dO_i
  * The same formulas hold in both modes (the implicit zeros act only
  * through Z).  O and lse are the outputs of spion_attn_fwd.  dQ, dK, dV use
- * the same layout and strides as Q.  ws_dev: >= spion_attn_workspace_bytes. */
+ * the same layout and strides as Q.  ws_dev: >= spion_attn_workspace_bytes
+ * (see above). */
 SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
                             const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev,
                             void *dV_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
@@ -205,6 +225,9 @@ SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, cons
  * pinned for asynchronous copies.  dev_arena: caller-owned device memory of
  * >= spion_step_arena_bytes(...) bytes.  Synchronises `stream` and returns
  * nnzb in *nnzb_host (may be NULL).
+ * Every parameter is validated before the first copy is enqueued; on an
+ * error after that point the call drains its copy streams and `stream`
+ * before returning, so no DMA touches the host buffers after it returns.
  * The (batch, head) range is processed in up to 16 contiguous chunks (>= 8 pairs and >= 4 MB per
  * input tensor each), pipelined:
  * the H2D copy of chunk c+1, the attention of chunk c (on `stream`) and the D2H
@@ -225,8 +248,7 @@ SPION_API spion_status spion_step_host(const float *scores_host, const void *Q_h
  * slices of softmax(scale Q K^T) — the attention score matrix averaged across
  * heads and batch — and, if sumsq_dev != NULL, *sumsq_dev = sum of A^2
  * (fp64), the square of the norm in Eq. 2 for Alg. 2's transition
- * test (host side: |d_{i-1} - d_i| < alpha with d_i = |sqrt(s_{i-1})
- * - sqrt(s_i)|).  Q, K: [bh][L][d] bf16 device, strides as spion_attn_fwd.
+ * test (spion_transition below).  Q, K: [bh][L][d] bf16 device, strides as spion_attn_fwd.
  * Needs d = 64, L % 128 == 0, L <= 8192 (else UNSUPPORTED).  ws_dev: >=
  * spion_score_mean_workspace_bytes(bh, L, d) bytes (a dense block pattern,
  * forward scratch and the row normalisers).  Tensor cores: the dense forward
@@ -236,6 +258,18 @@ SPION_API size_t spion_score_mean_workspace_bytes(int64_t bh, int32_t L, int32_t
 SPION_API spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, int32_t L, int32_t d,
                              int64_t stride_bh, int64_t stride_l, float scale, void *ws_dev, size_t ws_bytes,
                              float *A_dev, double *sumsq_dev, void *stream);
+
+/* Alg. 2's transition test with Eq. 2's distance, on
+ * the device in fp64: sumsq_dev[3] = sum (A^s)^2 of the score matrices of
+ * three consecutive dense-phase steps i-2, i-1, i (spion_score_mean);
+ * distance_k = | sqrt(sumsq[k-1]) - sqrt(sumsq[k]) |; *switch_dev = 1 if
+ * sqrt((distance_{i-1} - distance_i)^2) < alpha (switch to the sparse phase),
+ * else 0.  dist_dev (nullable): [2] = distance_{i-1}, distance_i.  alpha is
+ * the transition tolerance (reading Q10), finite and >= 0.  switch_host
+ * (nullable): also copied to the host (synchronises `stream`).  Stream-ordered
+ * otherwise, so it can sit inside a captured training step. */
+SPION_API spion_status spion_transition(const double *sumsq_dev, double alpha, int32_t *switch_dev,
+                                        double *dist_dev, int32_t *switch_host, void *stream);
 
 /* the sparse-MHA sub-layer around the attention (Alg. 5,
  * P:655-674).  The projections Q,K,V = X W^{Q,K,V} (l.2) and S W^O (l.9) are plain
@@ -259,6 +293,11 @@ SPION_API spion_status spion_dropout_residual(const void *y_dev, const void *e_d
 /* Number of this library's kernels launched by this thread since process
  * start (host-side counter, for the bench's gpu_launches claim). */
 SPION_API int64_t spion_launch_count(void);
+
+/* Number of tensor-core (tcgen05) attention kernels launched by this process
+ * (attn_fwd_tc_kernel, attn_bwd_*_tc_kernel): lets tests assert that the
+ * tensor-core path, not the CUDA-core path, ran. */
+SPION_API int64_t spion_tc_launch_count(void);
 
 /* Human-readable status. */
 SPION_API const char *spion_status_str(spion_status s);

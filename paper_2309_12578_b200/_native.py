@@ -11,6 +11,7 @@ SO_PATH = os.environ.get("SPION_LIB") or os.path.join(PKG, "lib", "libspion.so")
 OK = 0
 STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace", 6: "cuda", 7: "unsupported"}
 F32, BF16 = 0, 1
+PATH_CUDA_CORE, PATH_TCGEN05 = 0, 1  # spion_attn_path
 SOFTMAX = {"paper": 0, "masked": 1}
 THRESH = {"linear": 0, "nearest": 1, "absolute": 2}
 # spion_pattern_flags (include/spion.h): SPION-C, prose recursion, all-cells seeding
@@ -53,10 +54,14 @@ EXPORTS = {
     "spion_bsr_from_mask": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BSR),
                                            ctypes.c_void_p, ctypes.c_void_p]),
     "spion_attn_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int]),
+    "spion_attn_fwd_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                                         ctypes.c_int]),
+    "spion_attn_path": (ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.c_int, ctypes.POINTER(BSR)]),
     "spion_attn_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                       ctypes.c_int64, ctypes.c_int, ctypes.POINTER(BSR), ctypes.c_int, ctypes.c_float,
-                                      ctypes.c_void_p]),
+                                      ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "spion_attn_bwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
@@ -70,6 +75,9 @@ EXPORTS = {
                                                                 ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t,
                                                                 ctypes.c_void_p, ctypes.c_void_p]),
     "spion_launch_count": (ctypes.c_int64, []),
+    "spion_tc_launch_count": (ctypes.c_int64, []),
+    "spion_transition": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p]),
     "spion_status_str": (ctypes.c_char_p, [ctypes.c_int]),
 }
 

@@ -12,8 +12,9 @@
 #include "attn.cuh"
 
 namespace spion {
-static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_launches{0}, g_tc_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void note_tc_launch(int n) { g_tc_launches.fetch_add(n, std::memory_order_relaxed); }
 void report_cuda_error(cudaError_t e, const char *what, const char *file, int line) {
     static const bool on = getenv("SPION_DEBUG") != nullptr;
     if (on) fprintf(stderr, "[spion] %s:%d %s -> %s\n", file, line, what, cudaGetErrorString(e));
@@ -25,6 +26,7 @@ using namespace spion;
 extern "C" {
 
 int64_t spion_launch_count(void) { return (int64_t)g_launches.load(); }
+int64_t spion_tc_launch_count(void) { return (int64_t)g_tc_launches.load(); }
 
 // debug: copy the event trace of the last traced kernel (SPION_TRACE=1) to host:
 // 3 roles (producer, MMA, softmax thread 0) x 1024 (event, globaltimer) pairs
@@ -84,36 +86,32 @@ spion_status spion_pattern(const float *scores_dev, int32_t L, int32_t block, in
                                  out, nnzb_host, stream);
 }
 
-spion_status spion_pattern_variant(const float *scores_dev, int32_t L, int32_t block, int32_t filter,
-                                   double threshold, spion_threshold_kind kind, uint32_t variant, void *ws_dev,
-                                   size_t ws_bytes, spion_bsr *out, int32_t *nnzb_host, void *stream) {
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+// host-side validation of the pattern parameters and the threshold rank (Alg. 3 / P:600): the
+// order-statistic index lo (and whether the LINEAR interpolation fraction is positive) or the
+// absolute threshold in fixed point
+struct PatternParams {
+    long long lo = 0, T_abs = 0;
+    int frac_pos = 0;
+};
+static spion_status pattern_params(int32_t L, int32_t block, int32_t filter, double threshold,
+                                   spion_threshold_kind kind, uint32_t variant, PatternParams *pp) {
     if (variant & ~7u) return SPION_ERR_PARAM;
     if (L <= 0 || block <= 0 || L % block) return SPION_ERR_SHAPE;
     if (filter < 1 || filter % 2 == 0) return SPION_ERR_PARAM;
-    if (!scores_dev || !ws_dev) return SPION_ERR_PARAM;
-    if (!aligned16(scores_dev) || !aligned16(ws_dev) || L % 4) return SPION_ERR_ALIGN;
+    if (L % 4) return SPION_ERR_ALIGN;
     const int n = L / block;
     if (n > 128) return SPION_ERR_UNSUPPORTED;
     const int h = (filter - 1) / 2;
     if ((h + block - 1) / block > 63) return SPION_ERR_UNSUPPORTED;
-    if (ws_bytes < pattern_ws_bytes(L, block)) return SPION_ERR_WORKSPACE;
-    spion_status st = check_bsr_out(out, L, block);
-    if (st) return st;
-    out->L = L;
-    out->block = block;
-    out->nblk = n;
     const long long N = (long long)n * n;
-    long long lo = 0, T_abs = 0;
-    int frac_pos = 0;
     switch (kind) {
         case SPION_TH_QUANTILE_LINEAR: {
             if (!(threshold > 0.0 && threshold < 100.0)) return SPION_ERR_PARAM;
             const double hpos = ((double)(N - 1) * threshold) / 100.0;
-            lo = (long long)floor(hpos);
-            const double frac = hpos - (double)lo;
-            if (lo >= N - 1) { lo = N - 1; frac_pos = 0; }
-            else frac_pos = frac > 0.0;
+            pp->lo = (long long)floor(hpos);
+            const double frac = hpos - (double)pp->lo;
+            if (pp->lo >= N - 1) { pp->lo = N - 1; pp->frac_pos = 0; }
+            else pp->frac_pos = frac > 0.0;
             break;
         }
         case SPION_TH_QUANTILE_NEAREST: {
@@ -121,21 +119,40 @@ spion_status spion_pattern_variant(const float *scores_dev, int32_t L, int32_t b
             long long k = (long long)ceil(threshold / 100.0 * (double)N) - 1;
             if (k < 0) k = 0;
             if (k > N - 1) k = N - 1;
-            lo = k;
+            pp->lo = k;
             break;
         }
         case SPION_TH_ABSOLUTE: {
             if (!isfinite(threshold)) return SPION_ERR_PARAM;
             // gt(x) <=> x > t * B^2 * 2^32 (pool-mean units); x integral => x > floor(thr)
             const double thr = threshold * (double)((long long)block * block) * 4294967296.0;
-            if (thr < 0.0) T_abs = -1;
-            else if (thr >= 9.2e18) T_abs = 0x7fffffffffffffffLL;
-            else T_abs = (long long)floor(thr);
+            if (thr < 0.0) pp->T_abs = -1;
+            else if (thr >= 9.2e18) pp->T_abs = 0x7fffffffffffffffLL;
+            else pp->T_abs = (long long)floor(thr);
             break;
         }
         default: return SPION_ERR_PARAM;
     }
-    st = launch_pattern(scores_dev, L, block, filter, (int)kind, lo, frac_pos, (int)variant, T_abs, ws_dev, out, s);
+    return SPION_OK;
+}
+
+spion_status spion_pattern_variant(const float *scores_dev, int32_t L, int32_t block, int32_t filter,
+                                   double threshold, spion_threshold_kind kind, uint32_t variant, void *ws_dev,
+                                   size_t ws_bytes, spion_bsr *out, int32_t *nnzb_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PatternParams pp;
+    spion_status st = pattern_params(L, block, filter, threshold, kind, variant, &pp);
+    if (st) return st;
+    if (!scores_dev || !ws_dev) return SPION_ERR_PARAM;
+    if (!aligned16(scores_dev) || !aligned16(ws_dev)) return SPION_ERR_ALIGN;
+    if (ws_bytes < pattern_ws_bytes(L, block)) return SPION_ERR_WORKSPACE;
+    st = check_bsr_out(out, L, block);
+    if (st) return st;
+    out->L = L;
+    out->block = block;
+    out->nblk = L / block;
+    st = launch_pattern(scores_dev, L, block, filter, (int)kind, pp.lo, pp.frac_pos, (int)variant, pp.T_abs, ws_dev,
+                        out, s);
     if (st) return st;
     if (nnzb_host) {
         int flags = 0;
@@ -182,11 +199,21 @@ spion_status spion_bsr_from_mask(const uint8_t *mask_dev, int32_t L, int32_t blo
     return SPION_OK;
 }
 
+// attention workspace: [0, 256) the tensor-core kernels' work-item counters (zeroed by every call,
+// so concurrent calls sharing one pattern never share a counter); then, for the backward,
+// D_i = rowsum(dO * O) and -lse_i * log2(e), fp32 [bh][L] each
+static const size_t ATTN_CTR_BYTES = 256;
+
+size_t spion_attn_fwd_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt) {
+    (void)dt;
+    if (bh <= 0 || L <= 0 || d <= 0) return 0;
+    return ATTN_CTR_BYTES;
+}
+
 size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt) {
     (void)dt;
     if (bh <= 0 || L <= 0 || d <= 0) return 0;
-    // D_i = rowsum(dO * O) and -lse_i * log2(e) (the dK/dV kernel's exponent offset), fp32
-    return round_up((size_t)bh * L * 4, 256) * 2;
+    return ATTN_CTR_BYTES + round_up((size_t)bh * L * 4, 256) * 2;
 }
 
 static spion_status check_attn_common(const void *Q, const void *K, const void *V, int64_t bh, int32_t L,
@@ -229,20 +256,44 @@ static AttnArgs make_args(const void *Q, const void *K, const void *V, int64_t b
     return a;
 }
 
+// which kernels a call with these arguments runs (no launch); see spion_attn_path in spion.h
+static int attn_path(const AttnArgs &a, spion_dtype dt) {
+    if (dt == SPION_BF16 && tc_supported(a, dt)) return SPION_PATH_TCGEN05;
+    if (!simt_supported(a.B, a.d)) return -(int)SPION_ERR_UNSUPPORTED;
+    return SPION_PATH_CUDA_CORE;
+}
+
+int32_t spion_attn_path(int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
+                        const spion_bsr *pat) {
+    static const char dummy[16] __attribute__((aligned(16))) = {0};
+    spion_status st = check_attn_common(dummy, dummy, dummy, bh, L, d, stride_bh, stride_l, dt, pat, 0);
+    if (st) return -(int32_t)st;
+    if (bh > 65535) return -(int32_t)SPION_ERR_UNSUPPORTED;
+    AttnArgs a = make_args(dummy, dummy, dummy, bh, L, d, stride_bh, stride_l, pat, 0, 1.f);
+    return attn_path(a, dt);
+}
+
 spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, const void *V_dev, void *O_dev, float *lse_dev,
                             int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
-                            const spion_bsr *pat, spion_softmax_mode mode, float scale, void *stream) {
+                            const spion_bsr *pat, spion_softmax_mode mode, float scale, void *ws_dev,
+                            size_t ws_bytes, void *stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     spion_status st = check_attn_common(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, dt, pat, mode);
     if (st) return st;
-    if (!O_dev || !lse_dev) return SPION_ERR_PARAM;
-    if (!aligned16(O_dev) || !aligned16(lse_dev)) return SPION_ERR_ALIGN;
+    if (!O_dev || !lse_dev || !ws_dev) return SPION_ERR_PARAM;
+    if (!aligned16(O_dev) || !aligned16(lse_dev) || !aligned16(ws_dev)) return SPION_ERR_ALIGN;
+    if (ws_bytes < spion_attn_fwd_workspace_bytes(bh, L, d, dt)) return SPION_ERR_WORKSPACE;
     if (bh > 65535) return SPION_ERR_UNSUPPORTED;
     AttnArgs a = make_args(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, pat, mode, scale);
     a.Oout = O_dev;
     a.lse_out = lse_dev;
-    if (dt == SPION_BF16 && tc_supported(a, dt)) return launch_fwd_tc(a, s);
-    if (!simt_supported(a.B, d)) return SPION_ERR_UNSUPPORTED;
+    a.sched = static_cast<int *>(ws_dev);
+    const int path = attn_path(a, dt);
+    if (path < 0) return (spion_status)(-path);
+    if (path == SPION_PATH_TCGEN05) {
+        SPION_CUDA_TRY(cudaMemsetAsync(ws_dev, 0, ATTN_CTR_BYTES, s));
+        return launch_fwd_tc(a, s);
+    }
     return launch_fwd_simt(a, dt, s);
 }
 
@@ -267,11 +318,16 @@ spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_
     a.dQ = dQ_dev;
     a.dK = dK_dev;
     a.dV = dV_dev;
-    float *D = static_cast<float *>(ws_dev);
+    a.sched = static_cast<int *>(ws_dev);
+    float *D = reinterpret_cast<float *>(static_cast<char *>(ws_dev) + ATTN_CTR_BYTES);
     a.D = D;
-    a.nlse2 = reinterpret_cast<float *>(static_cast<char *>(ws_dev) + round_up((size_t)bh * L * 4, 256));
-    if (dt == SPION_BF16 && tc_supported(a, dt)) return launch_bwd_tc(a, s);
-    if (!simt_supported(a.B, d)) return SPION_ERR_UNSUPPORTED;
+    a.nlse2 = reinterpret_cast<float *>(static_cast<char *>(ws_dev) + ATTN_CTR_BYTES + round_up((size_t)bh * L * 4, 256));
+    const int path = attn_path(a, dt);
+    if (path < 0) return (spion_status)(-path);
+    if (path == SPION_PATH_TCGEN05) {
+        SPION_CUDA_TRY(cudaMemsetAsync(ws_dev, 0, ATTN_CTR_BYTES, s));
+        return launch_bwd_tc(a, s);
+    }
     st = launch_bwd_preprocess(a, dt, D, s);
     if (st) return st;
     return launch_bwd_simt(a, dt, s);
@@ -341,6 +397,7 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
                              float scale, void *dev_arena, size_t arena_bytes, int32_t *nnzb_host, void *stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (bh <= 0 || L <= 0 || d <= 0 || block <= 0 || L % block) return SPION_ERR_SHAPE;
+    if (!scores_host || !Q_host || !K_host || !V_host || !dO_host) return SPION_ERR_PARAM;
     if (!dev_arena || !aligned16(dev_arena)) return SPION_ERR_ALIGN;
     Arena A = arena_layout(bh, L, d, block, dt);
     if (arena_bytes < A.total) return SPION_ERR_WORKSPACE;
@@ -351,6 +408,31 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
     const int C = step_chunks(bh, t);
     const int64_t bhc = bh / C;
     const size_t tc = t / C, lc = (size_t)bhc * L * 4, wsc = spion_attn_workspace_bytes(bhc, L, d, dt);
+    spion_bsr bsr;
+    memset(&bsr, 0, sizeof(bsr));
+    bsr.L = L;
+    bsr.block = block;
+    bsr.nblk = n;
+    bsr.nnzb_cap = n * n;
+    bsr.brow_ptr = reinterpret_cast<int32_t *>(base + A.brow_ptr);
+    bsr.bcol_idx = reinterpret_cast<int32_t *>(base + A.bcol_idx);
+    bsr.bcol_ptr = reinterpret_cast<int32_t *>(base + A.bcol_ptr);
+    bsr.brow_idx = reinterpret_cast<int32_t *>(base + A.brow_idx);
+    bsr.mask = reinterpret_cast<uint8_t *>(base + A.mask);
+    bsr.nnzb = reinterpret_cast<int32_t *>(base + A.nnzb);
+    bsr.plan = base + A.plan;
+    bsr.plan_bytes = spion_bsr_plan_bytes(L, block);
+    // every parameter and shape check runs before the first copy is enqueued, so a rejected call
+    // never leaves DMA in flight on the caller's host buffers
+    {
+        PatternParams pp;
+        spion_status st = pattern_params(L, block, filter, threshold, kind, 0, &pp);
+        if (st) return st;
+        if (mode != SPION_SOFTMAX_PAPER && mode != SPION_SOFTMAX_MASKED) return SPION_ERR_PARAM;
+        const int32_t path = spion_attn_path(bhc, L, d, (int64_t)L * d, d, dt, &bsr);
+        if (path < 0) return (spion_status)(-path);
+        if (bhc > 65535) return SPION_ERR_UNSUPPORTED;
+    }
     // copy streams and events: created once per device and thread (the ABI's only state)
     constexpr int MAXC = 16;
     struct Pipe {
@@ -373,6 +455,22 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
         }
         P.dev = dev;
     }
+    // once a copy is enqueued, every exit drains both copy streams and the caller's stream
+    // first (the header promises a synchronised return; no DMA may outlive the call)
+    auto fail = [&](spion_status st) {
+        cudaStreamSynchronize(P.h2d);
+        cudaStreamSynchronize(P.d2h);
+        cudaStreamSynchronize(s);
+        return st;
+    };
+#define STEP_TRY(expr)                                                           \
+    do {                                                                         \
+        cudaError_t _e = (expr);                                                 \
+        if (_e != cudaSuccess) {                                                 \
+            ::spion::report_cuda_error(_e, #expr, __FILE__, __LINE__);           \
+            return fail(SPION_ERR_CUDA);                                         \
+        }                                                                        \
+    } while (0)
     auto H2D = [&](size_t off, const void *src, size_t bytes) {
         return cudaMemcpyAsync(base + off, src, bytes, cudaMemcpyHostToDevice, P.h2d);
     };
@@ -383,51 +481,42 @@ spion_status spion_step_host(const float *scores_host, const void *Q_host, const
     SPION_CUDA_TRY(cudaEventRecord(P.start, s));
     SPION_CUDA_TRY(cudaStreamWaitEvent(P.h2d, P.start, 0));
     SPION_CUDA_TRY(cudaStreamWaitEvent(P.d2h, P.start, 0));
-    SPION_CUDA_TRY(H2D(A.scores, scores_host, (size_t)L * L * 4));
-    SPION_CUDA_TRY(cudaEventRecord(P.scores, P.h2d));
+    STEP_TRY(H2D(A.scores, scores_host, (size_t)L * L * 4));
+    STEP_TRY(cudaEventRecord(P.scores, P.h2d));
     for (int c = 0; c < C; ++c) {
         const char *q = static_cast<const char *>(Q_host), *k = static_cast<const char *>(K_host);
         const char *v = static_cast<const char *>(V_host), *g = static_cast<const char *>(dO_host);
-        SPION_CUDA_TRY(H2D(A.Q + c * tc, q + c * tc, tc));
-        SPION_CUDA_TRY(H2D(A.K + c * tc, k + c * tc, tc));
-        SPION_CUDA_TRY(H2D(A.V + c * tc, v + c * tc, tc));
-        SPION_CUDA_TRY(H2D(A.dO + c * tc, g + c * tc, tc));
-        SPION_CUDA_TRY(cudaEventRecord(P.in[c], P.h2d));
+        STEP_TRY(H2D(A.Q + c * tc, q + c * tc, tc));
+        STEP_TRY(H2D(A.K + c * tc, k + c * tc, tc));
+        STEP_TRY(H2D(A.V + c * tc, v + c * tc, tc));
+        STEP_TRY(H2D(A.dO + c * tc, g + c * tc, tc));
+        STEP_TRY(cudaEventRecord(P.in[c], P.h2d));
     }
-    spion_bsr bsr;
-    memset(&bsr, 0, sizeof(bsr));
-    bsr.nnzb_cap = n * n;
-    bsr.brow_ptr = reinterpret_cast<int32_t *>(base + A.brow_ptr);
-    bsr.bcol_idx = reinterpret_cast<int32_t *>(base + A.bcol_idx);
-    bsr.bcol_ptr = reinterpret_cast<int32_t *>(base + A.bcol_ptr);
-    bsr.brow_idx = reinterpret_cast<int32_t *>(base + A.brow_idx);
-    bsr.mask = reinterpret_cast<uint8_t *>(base + A.mask);
-    bsr.nnzb = reinterpret_cast<int32_t *>(base + A.nnzb);
-    bsr.plan = base + A.plan;
-    bsr.plan_bytes = spion_bsr_plan_bytes(L, block);
-    SPION_CUDA_TRY(cudaStreamWaitEvent(s, P.scores, 0));
+    STEP_TRY(cudaStreamWaitEvent(s, P.scores, 0));
     spion_status st = spion_pattern(reinterpret_cast<const float *>(base + A.scores), L, block, filter, threshold,
                                     kind, base + A.pws, pattern_ws_bytes(L, block), &bsr, nullptr, stream);
-    if (st) return st;
+    if (st) return fail(st);
     for (int c = 0; c < C; ++c) {
         const size_t o = c * tc;
         float *lse = reinterpret_cast<float *>(base + A.lse + c * lc);
-        SPION_CUDA_TRY(cudaStreamWaitEvent(s, P.in[c], 0));
+        void *ws = base + A.aws + c * wsc;
+        STEP_TRY(cudaStreamWaitEvent(s, P.in[c], 0));
         st = spion_attn_fwd(base + A.Q + o, base + A.K + o, base + A.V + o, base + A.O + o, lse, bhc, L, d,
-                            (int64_t)L * d, d, dt, &bsr, mode, scale, stream);
-        if (st) return st;
+                            (int64_t)L * d, d, dt, &bsr, mode, scale, ws, wsc, stream);
+        if (st) return fail(st);
         st = spion_attn_bwd(base + A.Q + o, base + A.K + o, base + A.V + o, base + A.O + o, base + A.dO + o, lse,
                             base + A.dQ + o, base + A.dK + o, base + A.dV + o, bhc, L, d, (int64_t)L * d, d, dt, &bsr,
-                            mode, scale, base + A.aws + c * wsc, wsc, stream);
-        if (st) return st;
-        SPION_CUDA_TRY(cudaEventRecord(P.out[c], s));
-        SPION_CUDA_TRY(cudaStreamWaitEvent(P.d2h, P.out[c], 0));
-        if (O_host) SPION_CUDA_TRY(D2H(static_cast<char *>(O_host) + o, A.O + o, tc));
-        if (lse_host) SPION_CUDA_TRY(D2H(reinterpret_cast<char *>(lse_host) + c * lc, A.lse + c * lc, lc));
-        if (dQ_host) SPION_CUDA_TRY(D2H(static_cast<char *>(dQ_host) + o, A.dQ + o, tc));
-        if (dK_host) SPION_CUDA_TRY(D2H(static_cast<char *>(dK_host) + o, A.dK + o, tc));
-        if (dV_host) SPION_CUDA_TRY(D2H(static_cast<char *>(dV_host) + o, A.dV + o, tc));
+                            mode, scale, ws, wsc, stream);
+        if (st) return fail(st);
+        STEP_TRY(cudaEventRecord(P.out[c], s));
+        STEP_TRY(cudaStreamWaitEvent(P.d2h, P.out[c], 0));
+        if (O_host) STEP_TRY(D2H(static_cast<char *>(O_host) + o, A.O + o, tc));
+        if (lse_host) STEP_TRY(D2H(reinterpret_cast<char *>(lse_host) + c * lc, A.lse + c * lc, lc));
+        if (dQ_host) STEP_TRY(D2H(static_cast<char *>(dQ_host) + o, A.dQ + o, tc));
+        if (dK_host) STEP_TRY(D2H(static_cast<char *>(dK_host) + o, A.dK + o, tc));
+        if (dV_host) STEP_TRY(D2H(static_cast<char *>(dV_host) + o, A.dV + o, tc));
     }
+#undef STEP_TRY
     SPION_CUDA_TRY(cudaEventRecord(P.done, P.d2h));
     SPION_CUDA_TRY(cudaStreamWaitEvent(s, P.done, 0));
     int32_t nnzb = 0;
@@ -449,6 +538,7 @@ static size_t score_ws_layout(int64_t bh, int32_t L, size_t *o_pat, size_t *o_O,
                   spion_bsr_plan_bytes(L, 64));
     *o_O = take((size_t)bh * L * 64 * 2);
     *o_lse = take((size_t)bh * L * 4);
+    take(ATTN_CTR_BYTES);  // the dense forward's work-item counters (the last 256 bytes)
     return o;
 }
 
@@ -491,8 +581,9 @@ spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, 
     if (st) return st;
     bsr.mask = mask;
     float *lse = reinterpret_cast<float *>(base + o_lse);
+    const size_t total = score_ws_layout(bh, L, &o_pat, &o_O, &o_lse);
     st = spion_attn_fwd(Q_dev, K_dev, K_dev, base + o_O, lse, bh, L, d, stride_bh, stride_l, SPION_BF16, &bsr,
-                        SPION_SOFTMAX_MASKED, scale, stream);
+                        SPION_SOFTMAX_MASKED, scale, base + total - ATTN_CTR_BYTES, ATTN_CTR_BYTES, stream);
     if (st) return st;
     if (sumsq_dev) SPION_CUDA_TRY(cudaMemsetAsync(sumsq_dev, 0, sizeof(double), s));
     // partial tiles of a (batch, head)-split score pass reuse the forward's (dead) O scratch
@@ -500,6 +591,20 @@ spion_status spion_score_mean(const void *Q_dev, const void *K_dev, int64_t bh, 
     while (ks > 1 && (size_t)ks * L * L * 4 > (size_t)bh * L * 64 * 2) --ks;
     return launch_score_mean(Q_dev, K_dev, lse, bh, L, stride_bh, stride_l, scale, A_dev, sumsq_dev,
                              reinterpret_cast<float *>(base + o_O), ks, s);
+}
+
+spion_status spion_transition(const double *sumsq_dev, double alpha, int32_t *switch_dev, double *dist_dev,
+                              int32_t *switch_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!sumsq_dev || !switch_dev) return SPION_ERR_PARAM;
+    if (!(alpha >= 0.0) || !isfinite(alpha)) return SPION_ERR_PARAM;
+    spion_status st = launch_transition(sumsq_dev, alpha, switch_dev, dist_dev, s);
+    if (st) return st;
+    if (switch_host) {
+        SPION_CUDA_TRY(cudaMemcpyAsync(switch_host, switch_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SPION_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    return SPION_OK;
 }
 
 // ------------------------------------------------------------------ NEXT-4: sparse-MHA sub-layer

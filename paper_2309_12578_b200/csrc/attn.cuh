@@ -16,6 +16,7 @@ struct AttnArgs {
     float scale;
     const int *brow_ptr, *bcol_idx, *bcol_ptr, *brow_idx;
     const int *plan;
+    int *sched;  // tensor-core path: 4 zeroed work-item counters in the caller's workspace
 };
 
 extern unsigned long long *g_trace_buf;  // debug event trace (SPION_TRACE=1)
@@ -39,6 +40,8 @@ spion_status launch_score_mean(const void *Q, const void *K, const float *lse, i
                                int64_t stride_l, float scale, float *A, double *sumsq, float *part, int ks,
                                cudaStream_t s);
 int score_splits(int64_t bh, int L);
+// Alg. 2 / Eq. 2 transition test on three device sums of squares; scores.cu
+spion_status launch_transition(const double *sumsq, double alpha, int32_t *flag, double *dist, cudaStream_t s);
 
 // NEXT-4 sub-layer kernels; mha.cu
 spion_status launch_heads_permute(const void *src, void *dst, int64_t batch, int L, int W, int H, int d, int to_heads,

@@ -257,13 +257,10 @@ bool simt_supported(int B, int d) { return B >= 1 && d >= 1 && d <= 128 && dkdv_
 
 template <typename T>
 static spion_status set_attrs() {
-    static bool done = false;
-    if (!done) {
-        SPION_CUDA_TRY(allow_max_dyn_smem(attn_fwd_simt_kernel<T>));
-        SPION_CUDA_TRY(allow_max_dyn_smem(attn_dq_simt_kernel<T>));
-        SPION_CUDA_TRY(allow_max_dyn_smem(attn_dkdv_simt_kernel<T>));
-        done = true;
-    }
+    static PerDevice f0, f1, f2;
+    SPION_CUDA_TRY(smem_attr_once(f0, attn_fwd_simt_kernel<T>));
+    SPION_CUDA_TRY(smem_attr_once(f1, attn_dq_simt_kernel<T>));
+    SPION_CUDA_TRY(smem_attr_once(f2, attn_dkdv_simt_kernel<T>));
     return SPION_OK;
 }
 

@@ -155,7 +155,7 @@ struct TcParams {
     float scale, scale_log2;
     int off_ptr, off_col, off_msk;  // plan word offsets (row tiles: fptr/fcol/fmsk, column tiles: bptr/brow/bmsk)
     int off_order;                  // tiles in descending work order
-    int off_sched;                  // plan words [off_sched] item counter, [off_sched+1] done counter
+    int *sched;                     // caller workspace: this launch's work-item counter (zeroed per call)
     int off_heavy;                  // plan word: number of heavy tiles (scheduled first)
     int off_perm;                   // column tiles: plan word offset of bperm (slot -> block column)
     int G;                          // (batch, head) chunk of the scheduling order
@@ -187,12 +187,12 @@ __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
 }
 
 // ---------------------------------------------------------------- dynamic tile scheduler
-// Items (bh, tile) are handed out by an atomic counter in the plan, in chunks of G
+// Items (bh, tile) are handed out by an atomic counter in the caller's workspace (zeroed
+// by the host before every call, so launches sharing a pattern never share a counter), in chunks of G
 // (batch, head): within a chunk, tiles in descending order of work, each for all G
 // bh.  The producer warp fetches an item, stages its header and tile list in a
 // 4-slot shared ring, and signals `full`; the MMA thread and the 4 softmax warps
-// release the slot (`empty`, count 5) when they are done with the item.  The last
-// CTA to finish resets the counters, so every launch starts from zero.
+// release the slot (`empty`) when they are done with the item.
 struct Sched {
     int *hdr;  // [4][8]: item, bh, t, cnt, rc[0..3] (block-row counts of the slots)
     int *col;  // [4][SCHED_CAP]
@@ -242,7 +242,7 @@ __device__ __forceinline__ void sched_init(const Sched &sc, int consumers = 5) {
 // the next item's index from the plan's atomic counter (lane 0; the value is used by a later
 // sched_produce, so the atomic's round trip overlaps the current item's TMA issue)
 __device__ __forceinline__ int sched_prefetch(const TcParams &p) {
-    return (threadIdx.x & 31) == 0 ? atomicAdd(const_cast<int *>(p.plan) + p.off_sched, 1) : 0;
+    return (threadIdx.x & 31) == 0 ? atomicAdd(p.sched, 1) : 0;
 }
 
 // whole producer warp; returns the item (-1 = no more work).  pre: a prefetched item index
@@ -324,15 +324,6 @@ __device__ __forceinline__ void sched_finish(const TcParams &p, unsigned long lo
     if (p.trace && threadIdx.x == 0) {
         p.trace[16 + 8 * 2048 + 2 * blockIdx.x] = t_start;
         p.trace[16 + 8 * 2048 + 2 * blockIdx.x + 1] = gtimer();
-    }
-    if (threadIdx.x == 0) {
-        int *ctr = const_cast<int *>(p.plan) + p.off_sched;
-        __threadfence();
-        if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
-            atomicExch(ctr, 0);
-            atomicExch(ctr + 1, 0);
-            __threadfence();
-        }
     }
 }
 
@@ -1416,8 +1407,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // [bh][L][64] bf16 viewed as a 3-D tensor; box = 64 x box_rows x 1, 128-byte swizzle
 bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l, int box_rows);
-static bool make_map(CUtensorMap *m, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l,
-                     int box_rows) {
+static bool encode_map(CUtensorMap *m, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l,
+                       int box_rows) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[3] = {64, (cuuint64_t)L, (cuuint64_t)bh};
@@ -1428,6 +1419,36 @@ static bool make_map(CUtensorMap *m, const void *base, int L, int64_t bh, int64_
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+// Tensor maps are pure functions of (address, shape, strides, box), so encoded maps are cached per
+// host thread (a small round-robin table): a step that re-launches on the same buffers encodes
+// nothing (the backward needs ten maps per call).
+static bool make_map(CUtensorMap *m, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l,
+                     int box_rows) {
+    struct Entry {
+        const void *base;
+        int64_t bh, stride_bh, stride_l;
+        int L, box_rows;
+        alignas(64) CUtensorMap map;
+    };
+    constexpr int CAP = 48;
+    static thread_local Entry cache[CAP];
+    static thread_local int used = 0, next = 0;
+    for (int i = 0; i < used; ++i) {
+        const Entry &e = cache[i];
+        if (e.base == base && e.L == L && e.bh == bh && e.stride_bh == stride_bh && e.stride_l == stride_l &&
+            e.box_rows == box_rows) {
+            *m = e.map;
+            return true;
+        }
+    }
+    if (!encode_map(m, base, L, bh, stride_bh, stride_l, box_rows)) return false;
+    Entry &e = cache[next];
+    e.base = base; e.bh = bh; e.stride_bh = stride_bh; e.stride_l = stride_l; e.L = L; e.box_rows = box_rows;
+    e.map = *m;
+    next = (next + 1) % CAP;
+    if (used < CAP) ++used;
+    return true;
 }
 
 bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l, int box_rows) {
@@ -1445,14 +1466,14 @@ bool tc_supported(const AttnArgs &a, spion_dtype dt) {
 
 unsigned long long *g_trace_buf = nullptr;
 static int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+    static int n[64] = {0};
+    const int dev = current_device() & 63;
+    if (!n[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
     }
-    return n;
+    return n[dev];
 }
 
 // which: 0 fwd (row tiles), 1 dq (row tiles), 2 dkdv (column tiles)
@@ -1477,7 +1498,7 @@ static TcParams base_params(const AttnArgs &a, int which, int ctas) {
     p.off_col = (int)(rows ? pl.fcol : pl.brow);
     p.off_msk = (int)(rows ? pl.fmsk : pl.bmsk);
     p.off_order = (int)(rows ? pl.forder : pl.border);
-    p.off_sched = 8 + 2 * which;
+    p.sched = a.sched + which;
     p.off_heavy = rows ? 5 : 6;
     p.off_perm = rows ? 0 : (int)pl.bperm;
     const int grid = ctas * num_sms();
@@ -1509,11 +1530,8 @@ static int grid_for(const TcParams &p, int ctas) {
 
 template <int B>
 static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem<B>()));
-        attr = true;
-    }
+    static PerDevice attr;
+    SPION_CUDA_TRY(smem_attr_once(attr, attn_fwd_tc_kernel<B>, (int)fwd_smem<B>()));
     CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mk, a.K, a.L, a.bh, a.stride_bh, a.stride_l, B) ||
@@ -1525,17 +1543,15 @@ static spion_status fwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     p.lse_out = a.lse_out;
     attn_fwd_tc_kernel<B><<<grid_for(p, Cfg<B>::FWD_CTAS), TC_THREADS, fwd_smem<B>(), s>>>(mq, mk, mv, mo, p);
     SPION_LAUNCH_CHECK();
+    note_tc_launch();
     return SPION_OK;
 }
 
 template <int B>
 static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dq_smem<B>()));
-        SPION_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dkv_smem<B>()));
-        attr = true;
-    }
+    static PerDevice attr_dq, attr_dkv;
+    SPION_CUDA_TRY(smem_attr_once(attr_dq, attn_bwd_dq_tc_kernel<B>, (int)dq_smem<B>()));
+    SPION_CUDA_TRY(smem_attr_once(attr_dkv, attn_bwd_dkdv_tc_kernel<B>, (int)dkv_smem<B>()));
     CUtensorMap mq128, mdo128, mo128, mkB, mvB, mqB, mdoB, mdq128, mdkB, mdvB;
     if (!make_map(&mq128, a.Q, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
         !make_map(&mdo128, a.dO, a.L, a.bh, a.stride_bh, a.stride_l, 128) ||
@@ -1566,6 +1582,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), bwd_threads(Cfg<B>::DKV_MW, Cfg<B>::DKV_NSW), dkv_smem<B>(), s>>>(
         mkB, mvB, mqB, mdoB, mdkB, mdvB, q);
     SPION_LAUNCH_CHECK();
+    note_tc_launch(2);
     return SPION_OK;
 }
 

@@ -4,12 +4,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "spion.h"
 
 namespace spion {
 
 // host-side launch counter (spion_launch_count)
 void note_launch(int n = 1);
+// host-side counter of tensor-core (tcgen05) attention kernel launches (spion_tc_launch_count)
+void note_tc_launch(int n = 1);
 
 // SPION_DEBUG=1 in the environment prints the failing CUDA call
 void report_cuda_error(cudaError_t e, const char *what, const char *file, int line);
@@ -45,6 +49,27 @@ static inline cudaError_t allow_max_dyn_smem(F *func) {
     e = cudaFuncGetAttributes(&fa, func);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
+// "done once per device" flags: kernel attributes (e.g. the dynamic shared memory limit) belong
+// to the current device's context, so a process driving several GPUs sets them once per device
+struct PerDevice {
+    std::atomic<unsigned long long> bits{0};
+};
+static inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+// raise func's dynamic shared memory limit to `bytes` (or the device maximum, bytes < 0) once per device
+template <typename F>
+static inline cudaError_t smem_attr_once(PerDevice &flag, F *func, int bytes = -1) {
+    const unsigned long long bit = 1ull << (current_device() & 63);
+    if (flag.bits.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    cudaError_t e = bytes < 0 ? allow_max_dyn_smem(func)
+                              : cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) flag.bits.fetch_or(bit, std::memory_order_release);
+    return e;
 }
 
 static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -93,7 +118,8 @@ struct PlanLayout {
     // header words: [0] n [1] S [2] ntiles [3] fwd entries [4] bwd entries
     //               [5] heavy row tiles [6] heavy column tiles (prefixes of the work orders)
     //               [7] heavy block columns (> 2x the mean count; a prefix of bperm)
-    //               [8] fwd item counter [9] fwd done [10] bwd item counter [11] bwd done
+    //               [8..15] reserved (the attention kernels' work-item counters live in the
+    //               caller's attention workspace, not in the shared pattern)
     size_t fptr, bptr, forder, border, fcol, fmsk, brow, bmsk, bperm, words;
     __host__ __device__ PlanLayout(int n_, int block) {
         n = n_;

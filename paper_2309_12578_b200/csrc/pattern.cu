@@ -269,11 +269,8 @@ static size_t k1_smem_bytes(const K1Geom &g) {
 template <int K4>
 static spion_status k1_launch(const float *scores, const K1Geom &g, unsigned long long *pool, int *flags,
                               cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        SPION_CUDA_TRY(allow_max_dyn_smem(pattern_pool_kernel<K4>));
-        attr = true;
-    }
+    static PerDevice attr;
+    SPION_CUDA_TRY(smem_attr_once(attr, pattern_pool_kernel<K4>));
     const int n = g.L / g.B;
     const int rs = (g.B + g.RP - 1) / g.RP;
     pattern_pool_kernel<K4><<<dim3(g.n_cc, n, rs), K1_WARPS * 32, k1_smem_bytes<K4>(g), s>>>(scores, g, pool, flags);
@@ -862,11 +859,8 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     }
     const size_t smem2 = k2_smem_bytes(n, true);
     if (smem2 > 227 * 1024) return SPION_ERR_UNSUPPORTED;
-    static bool attr2 = false;
-    if (!attr2) {
-        SPION_CUDA_TRY(allow_max_dyn_smem(pattern_finalize_kernel));
-        attr2 = true;
-    }
+    static PerDevice attr2;
+    SPION_CUDA_TRY(smem_attr_once(attr2, pattern_finalize_kernel));
     pattern_finalize_kernel<<<1, K2_THREADS, smem2, s>>>(a);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
@@ -889,11 +883,8 @@ spion_status launch_bsr_from_mask(const uint8_t *mask, int L, int B, spion_bsr *
     a.nnzb_cap = out->nnzb_cap;
     a.plan = reinterpret_cast<int *>(out->plan);
     const size_t smem = k2_smem_bytes(n, false);
-    static bool attr = false;
-    if (!attr) {
-        SPION_CUDA_TRY(allow_max_dyn_smem(bsr_from_mask_kernel));
-        attr = true;
-    }
+    static PerDevice attr;
+    SPION_CUDA_TRY(smem_attr_once(attr, bsr_from_mask_kernel));
     bsr_from_mask_kernel<<<1, K2_THREADS, smem, s>>>(mask, a);
     SPION_LAUNCH_CHECK();
     return SPION_OK;

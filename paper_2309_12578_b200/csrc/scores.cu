@@ -174,11 +174,8 @@ spion_status launch_score_mean(const void *Q, const void *K, const float *lse, i
     if (!tc_make_map(&mq, Q, L, bh, stride_bh, stride_l, 128) || !tc_make_map(&mk, K, L, bh, stride_bh, stride_l, 128))
         return SPION_ERR_CUDA;
     const size_t smem = 1024 + 2 * SM_NST * SM_TILE + 256;
-    static bool attr = false;
-    if (!attr) {
-        SPION_CUDA_TRY(cudaFuncSetAttribute(score_mean_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    static PerDevice attr;
+    SPION_CUDA_TRY(smem_attr_once(attr, score_mean_tc_kernel, (int)smem));
     if (ks < 1 || !part) ks = 1;
     const float inv = 1.f / (float)bh;
     score_mean_tc_kernel<<<dim3(L / 128, L / 128, ks), SM_THREADS, smem, s>>>(
@@ -191,6 +188,28 @@ spion_status launch_score_mean(const void *Q, const void *K, const float *lse, i
                                                    reinterpret_cast<float4 *>(A), sumsq);
         SPION_LAUNCH_CHECK();
     }
+    return SPION_OK;
+}
+
+// Alg. 2 with Eq. 2, one thread in fp64: with s_k = sum (A^s_k)^2 of three
+// consecutive dense-phase score matrices, distance_k = | sqrt(s_{k-1}) - sqrt(s_k) |, and the
+// training switches to the sparse phase when sqrt((distance_{i-1} - distance_i)^2) < alpha
+// (reading Q10: this alpha is the transition tolerance, not the quantile).  Device-side, so the
+// test needs no host round trip inside a captured training step.
+__global__ void transition_kernel(const double *ss, double alpha, int32_t *flag, double *dist) {
+    const double d1 = fabs(sqrt(ss[0]) - sqrt(ss[1]));
+    const double d2 = fabs(sqrt(ss[1]) - sqrt(ss[2]));
+    const double g = d1 - d2;
+    *flag = sqrt(g * g) < alpha ? 1 : 0;
+    if (dist) {
+        dist[0] = d1;
+        dist[1] = d2;
+    }
+}
+
+spion_status launch_transition(const double *sumsq, double alpha, int32_t *flag, double *dist, cudaStream_t s) {
+    transition_kernel<<<1, 1, 0, s>>>(sumsq, alpha, flag, dist);
+    SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
 

@@ -72,8 +72,12 @@ class _DropoutResidual(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, y, e, p: float, seed: int):
-        out = torch.empty_like(e)
-        st = N.lib().spion_dropout_residual(spion._p(y.contiguous()), spion._p(e.contiguous()), spion._p(out), out.numel(),
+        if y.dtype != torch.bfloat16 or e.dtype != torch.bfloat16 or y.numel() != e.numel():
+            raise ValueError("dropout_residual: y and e must be bf16 with the same number of elements")
+        # bind the contiguous copies to locals: they must outlive the (asynchronous) kernel launch
+        yc, ec = y.contiguous(), e.contiguous()
+        out = torch.empty_like(ec)
+        st = N.lib().spion_dropout_residual(spion._p(yc), spion._p(ec), spion._p(out), out.numel(),
                                             float(p), int(seed), spion._stream(y.device))
         N.check(st, "spion_dropout_residual")
         ctx.p, ctx.seed = p, seed

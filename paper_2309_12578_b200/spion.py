@@ -9,6 +9,7 @@ PyTorch fallback: a missing library or a non-CUDA tensor raises.
     o, lse = attn_fwd(q, k, v, bsr)                            # Alg. 5/6, Eq. 5
     dq, dk, dv = attn_bwd(q, k, v, o, do, lse, bsr)            # custom autograd
     o = attention(q, k, v, bsr)                                # autograd.Function
+    attn_path(q, bsr) -> "tcgen05" | "cuda_core"               # which kernels run
 """
 from __future__ import annotations
 
@@ -156,8 +157,11 @@ def _layout(q: torch.Tensor):
 
 
 def attn_fwd(q, k, v, bp: BlockPattern, mode: str = "paper", scale: Optional[float] = None,
-             out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None):
-    """O, lse of block-sparse attention (Eq. 5 / Alg. 6).  q,k,v: [bh][L][d], same strides."""
+             out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+             workspace: Optional[torch.Tensor] = None):
+    """O, lse of block-sparse attention (Eq. 5 / Alg. 6).  q,k,v: [bh][L][d], same strides.
+    ``workspace``: >= spion_attn_fwd_workspace_bytes (the kernels' work-item counters); one per
+    concurrently running call (allocated per call when omitted)."""
     _require_cuda(q, k, v)
     bh, L, d, sb, sl = _layout(q)
     if k.stride() != q.stride() or v.stride() != q.stride() or k.shape != q.shape or v.shape != q.shape:
@@ -168,11 +172,32 @@ def attn_fwd(q, k, v, bp: BlockPattern, mode: str = "paper", scale: Optional[flo
         out = torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device)
     if lse is None:
         lse = torch.empty((bh, L), dtype=torch.float32, device=q.device)
+    lib = N.lib()
+    if workspace is None:
+        nb = lib.spion_attn_fwd_workspace_bytes(bh, L, d, _dtype_code(q))
+        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=q.device)
     s = bp.c_struct()
-    st = N.lib().spion_attn_fwd(_p(q), _p(k), _p(v), _p(out), _p(lse), bh, L, d, sb, sl, _dtype_code(q),
-                                ctypes.byref(s), N.SOFTMAX[mode], float(scale), _stream(q.device))
+    st = lib.spion_attn_fwd(_p(q), _p(k), _p(v), _p(out), _p(lse), bh, L, d, sb, sl, _dtype_code(q),
+                            ctypes.byref(s), N.SOFTMAX[mode], float(scale), _p(workspace), workspace.numel(),
+                            _stream(q.device))
     N.check(st, "spion_attn_fwd")
     return out, lse
+
+
+def attn_path(q: torch.Tensor, bp: BlockPattern) -> str:
+    """Which kernels attn_fwd / attn_bwd run for q's shape and layout and this pattern:
+    "tcgen05" (tensor cores), "cuda_core", or raises if the call would be rejected."""
+    bh, L, d, sb, sl = _layout(q)
+    s = bp.c_struct()
+    r = N.lib().spion_attn_path(bh, L, d, sb, sl, _dtype_code(q), ctypes.byref(s))
+    if r < 0:
+        N.check(-r, "spion_attn_path")
+    return "tcgen05" if r == N.PATH_TCGEN05 else "cuda_core"
+
+
+def tc_launch_count() -> int:
+    """Tensor-core attention kernels launched by this process (host counter)."""
+    return int(N.lib().spion_tc_launch_count())
 
 
 def attn_workspace(bh: int, L: int, d: int, dtype, device) -> torch.Tensor:
@@ -215,7 +240,8 @@ class _SparseAttention(torch.autograd.Function):
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse = ctx.saved_tensors
-        do = do.contiguous() if do.stride() != q.stride() else do
+        if do.stride() != q.stride():  # the kernels take one layout for every tensor: materialise q's
+            do = torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device).copy_(do)
         dq, dk, dv = attn_bwd(q, k, v, o, do, lse, ctx.bp, ctx.mode, ctx.scale)
         return dq, dk, dv, None, None, None
 
@@ -230,9 +256,12 @@ def launch_count() -> int:
 
 
 # ------------------------------------------------------------------ NEXT-1: dense-phase scores
-def score_mean(q: torch.Tensor, k: torch.Tensor, scale: Optional[float] = None, out: Optional[torch.Tensor] = None):
+def score_mean(q: torch.Tensor, k: torch.Tensor, scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+               sumsq: Optional[torch.Tensor] = None):
     """A^s = mean over (batch, head) of softmax(scale q k^T) as fp32 [L][L], and sum(A^2)
-    (Eq. 2's squared norm) as a python float.  q, k: [bh][L][64] bf16 (device)."""
+    (Eq. 2's squared norm) as a python float.  q, k: [bh][L][64] bf16 (device).  With ``sumsq`` (a
+    one-element device float64 tensor, e.g. a slot of transition()'s input) the sum is written
+    there and returned as that tensor, without a host sync."""
     _require_cuda(q, k)
     bh, L, d = q.shape
     scale = 1.0 / math.sqrt(d) if scale is None else scale
@@ -240,17 +269,28 @@ def score_mean(q: torch.Tensor, k: torch.Tensor, scale: Optional[float] = None, 
     nb = lib.spion_score_mean_workspace_bytes(bh, L, d)
     ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=q.device)
     A = out if out is not None else torch.empty((L, L), dtype=torch.float32, device=q.device)
-    ss = torch.zeros(1, dtype=torch.float64, device=q.device)
+    ss = sumsq if sumsq is not None else torch.zeros(1, dtype=torch.float64, device=q.device)
+    if ss.dtype != torch.float64 or not ss.is_cuda:
+        raise ValueError("sumsq must be a device float64 tensor")
     st = lib.spion_score_mean(_p(q), _p(k), bh, L, d, q.stride(0), q.stride(1), scale, _p(ws), nb, _p(A), _p(ss),
                               _stream(q.device))
     N.check(st, "spion_score_mean")
-    return A, float(ss.item())
+    return A, (ss if sumsq is not None else float(ss.item()))
 
 
-def transition(sumsq_im2: float, sumsq_im1: float, sumsq_i: float, alpha: float) -> bool:
-    """Alg. 2 with Eq. 2: distance_i = |sqrt(sum A_{i-1}^2) - sqrt(sum A_i^2)|; switch to the
-    sparse phase when |distance_{i-1} - distance_i| < alpha.  Host arithmetic on three norms."""
-    d1 = abs(math.sqrt(sumsq_im2) - math.sqrt(sumsq_im1))
-    d2 = abs(math.sqrt(sumsq_im1) - math.sqrt(sumsq_i))
-    return abs(d1 - d2) < alpha
-
+def transition(sumsq: torch.Tensor, alpha: float, sync: bool = True):
+    """Alg. 2 with Eq. 2 through spion_transition: ``sumsq`` is a device fp64
+    tensor [3] of sum((A^s)^2) for dense-phase steps i-2, i-1, i (from score_mean).  Returns
+    (switch, distances) — switch is a python bool when ``sync`` else a device int32 [1]; distances a
+    device fp64 [2] = (distance_{i-1}, distance_i)."""
+    _require_cuda(sumsq)
+    if sumsq.dtype != torch.float64 or sumsq.numel() != 3:
+        raise ValueError("sumsq must be a device float64 tensor of 3 sums of squares")
+    sumsq = sumsq.contiguous()
+    flag = torch.zeros(1, dtype=torch.int32, device=sumsq.device)
+    dist = torch.empty(2, dtype=torch.float64, device=sumsq.device)
+    host = ctypes.c_int32(0)
+    st = N.lib().spion_transition(_p(sumsq), float(alpha), _p(flag), _p(dist), ctypes.byref(host) if sync else None,
+                                  _stream(sumsq.device))
+    N.check(st, "spion_transition")
+    return (bool(host.value) if sync else flag), dist

@@ -84,17 +84,64 @@ def test_attention_rejects_bad_arguments():
     s.L, s.block, s.nblk = 64, 8, 8
     P = ctypes.c_void_p(256)
     # d > 128
-    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 256, 64 * 256, 256, N.F32, ctypes.byref(s), 0, 1.0, None) == 1
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 256, 64 * 256, 256, N.F32, ctypes.byref(s), 0, 1.0, P, 256, None) == 1
     # pattern for another L
-    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 128, 16, 128 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0, None) == 1
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 128, 16, 128 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0, P, 256, None) == 1
     # bad mode / dtype
-    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 5, 1.0, None) == 2
-    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, 7, ctypes.byref(s), 0, 1.0, None) == 2
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 5, 1.0, P, 256, None) == 2
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, 7, ctypes.byref(s), 0, 1.0, P, 256, None) == 2
     # misaligned stride for bf16
-    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 20, 20, N.BF16, ctypes.byref(s), 0, 1.0, None) == 4
-    # workspace too small
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 20, 20, N.BF16, ctypes.byref(s), 0, 1.0, P, 256, None) == 4
+    # workspace too small (forward: the 256-byte counter area; backward: counters + D + -lse*log2e)
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0, P, 16,
+                              None) == 5
+    assert lib.spion_attn_fwd(P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0, None, 256,
+                              None) == 2
     assert lib.spion_attn_bwd(P, P, P, P, P, P, P, P, P, 1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s), 0, 1.0,
                               P, 16, None) == 5
+
+
+def test_attn_path_query():
+    """spion_attn_path is host-only: which kernel family a call would run, or -status."""
+    lib = N.lib()
+    s = _bsr_dummy(64, 8)
+    s.L, s.block, s.nblk = 64, 8, 8
+    assert lib.spion_attn_path(1, 64, 16, 64 * 16, 16, N.F32, ctypes.byref(s)) == N.PATH_CUDA_CORE
+    assert lib.spion_attn_path(1, 64, 256, 64 * 256, 256, N.F32, ctypes.byref(s)) == -1   # d > 128: shape
+    assert lib.spion_attn_path(1, 64, 16, 64 * 20, 20, N.BF16, ctypes.byref(s)) == -4     # stride % 8: align
+    t = _bsr_dummy(4096, 64)
+    t.L, t.block, t.nblk = 4096, 64, 64
+    # bf16 d=64 B=64 without a plan cannot take the tensor-core path
+    assert lib.spion_attn_path(128, 4096, 64, 4096 * 64, 64, N.BF16, ctypes.byref(t)) == N.PATH_CUDA_CORE
+    t.plan, t.plan_bytes = 256, lib.spion_bsr_plan_bytes(4096, 64)
+    # with a plan: tcgen05 where the driver entry point exists (GPU box), else the CUDA-core path
+    assert lib.spion_attn_path(128, 4096, 64, 4096 * 64, 64, N.BF16, ctypes.byref(t)) in (N.PATH_CUDA_CORE,
+                                                                                         N.PATH_TCGEN05)
+    assert lib.spion_attn_fwd_workspace_bytes(128, 4096, 64, N.BF16) == 256
+    assert lib.spion_attn_workspace_bytes(128, 4096, 64, N.BF16) == 256 + 2 * 128 * 4096 * 4
+
+
+def test_transition_rejects_bad_arguments():
+    lib = N.lib()
+    P = ctypes.c_void_p(256)
+    assert lib.spion_transition(None, 0.1, P, None, None, None) == 2
+    assert lib.spion_transition(P, 0.1, None, None, None, None) == 2
+    assert lib.spion_transition(P, float("nan"), P, None, None, None) == 2
+    assert lib.spion_transition(P, -1.0, P, None, None, None) == 2
+
+
+def test_step_host_validates_before_copying():
+    """Parameter errors come back before any copy is enqueued (the host pointers are bogus)."""
+    lib = N.lib()
+    P = ctypes.c_void_p(256)
+    nb = lib.spion_step_arena_bytes(2, 64, 16, 8, N.F32)
+    args = [P] * 10
+    # even filter, alpha out of range, bad mode: all rejected synchronously, no CUDA call needed
+    assert lib.spion_step_host(*args, 2, 64, 16, 8, 30, 75.0, 0, N.F32, 0, 0.25, P, nb, None, None) == 2
+    assert lib.spion_step_host(*args, 2, 64, 16, 8, 31, 100.0, 0, N.F32, 0, 0.25, P, nb, None, None) == 2
+    assert lib.spion_step_host(*args, 2, 64, 16, 8, 31, 75.0, 0, N.F32, 9, 0.25, P, nb, None, None) == 2
+    assert lib.spion_step_host(*args, 2, 64, 256, 8, 31, 75.0, 0, N.F32, 0, 0.25, P,
+                               lib.spion_step_arena_bytes(2, 64, 256, 8, N.F32), None, None) == 1
 
 
 def test_status_strings():
