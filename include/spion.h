@@ -211,12 +211,28 @@ SPION_API spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, cons
  * The same formulas hold in both modes (the implicit zeros act only
  * through Z).  O and lse are the outputs of spion_attn_fwd.  dQ, dK, dV use
  * the same layout and strides as Q.  ws_dev: >= spion_attn_workspace_bytes
- * (see above). */
+ * (see above).
+ * Tensor-core path: block 64 runs ONE fused pass over the pattern's column
+ * tiles (dK, dV accumulated per tile; dQ accumulated in fp32 in the
+ * workspace by bulk reduce-adds at L2, so its summation order depends on
+ * scheduling: dQ may differ between runs by rounding); block 32 (and block
+ * 64 with SPION_BWD_DETERMINISTIC) runs a row pass for dQ and a column pass
+ * for dK/dV, atomic-free and bitwise reproducible. */
 SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
                             const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev,
                             void *dV_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
                             int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,
                             float scale, void *ws_dev, size_t ws_bytes, void *stream);
+
+/* spion_attn_bwd with flags (bitwise OR; other bits: SPION_ERR_PARAM):
+ * SPION_BWD_DETERMINISTIC — bitwise reproducible results (the two-pass
+ * tensor-core backward at every block size). */
+typedef enum { SPION_BWD_DETERMINISTIC = 1 } spion_bwd_flags;
+SPION_API spion_status spion_attn_bwd_ex(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
+                            const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev,
+                            void *dV_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
+                            int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,
+                            float scale, uint32_t flags, void *ws_dev, size_t ws_bytes, void *stream);
 
 /* One whole step of the hot path from HOST buffers (the end-to-end call):
  * copies scores, Q, K, V, dO host->device, runs spion_pattern,

@@ -12,6 +12,7 @@ OK = 0
 STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace", 6: "cuda", 7: "unsupported"}
 F32, BF16 = 0, 1
 PATH_CUDA_CORE, PATH_TCGEN05 = 0, 1  # spion_attn_path
+BWD_DETERMINISTIC = 1  # spion_attn_bwd_ex flags
 SOFTMAX = {"paper": 0, "masked": 1}
 THRESH = {"linear": 0, "nearest": 1, "absolute": 2}
 # spion_pattern_flags (include/spion.h): SPION-C, prose recursion, all-cells seeding
@@ -67,6 +68,12 @@ EXPORTS = {
                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                       ctypes.c_int64, ctypes.c_int, ctypes.POINTER(BSR), ctypes.c_int, ctypes.c_float,
                                       ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "spion_attn_bwd_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(BSR),
+                                         ctypes.c_int, ctypes.c_float, ctypes.c_uint32, ctypes.c_void_p,
+                                         ctypes.c_size_t, ctypes.c_void_p]),
     "spion_step_arena_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                                  ctypes.c_int]),
     "spion_step_host": (ctypes.c_int, [ctypes.c_void_p] * 10 + [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,

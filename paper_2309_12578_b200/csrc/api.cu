@@ -210,10 +210,21 @@ size_t spion_attn_fwd_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dt
     return ATTN_CTR_BYTES;
 }
 
+// bf16 d = 64 (the tensor-core envelope) also reserves the fused backward's fp32 dQ accumulator
+// and per-(bh, query block) completion counters (sized for the smallest block, 32)
+static size_t attn_ws_base(int64_t bh, int32_t L) { return ATTN_CTR_BYTES + round_up((size_t)bh * L * 4, 256) * 2; }
+
 size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype dt) {
-    (void)dt;
     if (bh <= 0 || L <= 0 || d <= 0) return 0;
-    return ATTN_CTR_BYTES + round_up((size_t)bh * L * 4, 256) * 2;
+    size_t b = attn_ws_base(bh, L);
+    if (dt == SPION_BF16 && d == 64) b += fused_bwd_ws_bytes(bh, L, (L + 31) / 32);
+    return b;
+}
+
+// SPION_SPLIT_BWD=1: the two-kernel (dQ row pass + dK/dV column pass) backward at B = 64 too
+static bool split_bwd_forced() {
+    static const int v = getenv("SPION_SPLIT_BWD") != nullptr;
+    return v != 0;
 }
 
 static spion_status check_attn_common(const void *Q, const void *K, const void *V, int64_t bh, int32_t L,
@@ -302,6 +313,16 @@ spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_
                             int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
                             const spion_bsr *pat, spion_softmax_mode mode, float scale, void *ws_dev,
                             size_t ws_bytes, void *stream) {
+    return spion_attn_bwd_ex(Q_dev, K_dev, V_dev, O_dev, dO_dev, lse_dev, dQ_dev, dK_dev, dV_dev, bh, L, d, stride_bh,
+                             stride_l, dt, pat, mode, scale, 0u, ws_dev, ws_bytes, stream);
+}
+
+spion_status spion_attn_bwd_ex(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
+                               const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev, void *dV_dev,
+                               int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
+                               const spion_bsr *pat, spion_softmax_mode mode, float scale, uint32_t flags,
+                               void *ws_dev, size_t ws_bytes, void *stream) {
+    if (flags & ~(uint32_t)SPION_BWD_DETERMINISTIC) return SPION_ERR_PARAM;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     spion_status st = check_attn_common(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, dt, pat, mode);
     if (st) return st;
@@ -326,6 +347,8 @@ spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_
     if (path < 0) return (spion_status)(-path);
     if (path == SPION_PATH_TCGEN05) {
         SPION_CUDA_TRY(cudaMemsetAsync(ws_dev, 0, ATTN_CTR_BYTES, s));
+        if (fused_bwd_supported(a) && !split_bwd_forced() && !(flags & SPION_BWD_DETERMINISTIC))
+            return launch_bwd_fused(a, static_cast<char *>(ws_dev) + attn_ws_base(bh, L), s);
         return launch_bwd_tc(a, s);
     }
     st = launch_bwd_preprocess(a, dt, D, s);

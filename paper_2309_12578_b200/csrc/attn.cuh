@@ -32,6 +32,12 @@ bool tc_supported(const AttnArgs &a, spion_dtype dt);
 spion_status launch_fwd_tc(const AttnArgs &a, cudaStream_t s);
 spion_status launch_bwd_tc(const AttnArgs &a, cudaStream_t s);
 
+// fused tensor-core backward (B = 64, d = 64; dQ by bulk reduce-add); attn_bwd_fused.cu.
+// fws: >= fused_bwd_ws_bytes(bh, L, n) bytes (completion counters + the fp32 dQ accumulator)
+bool fused_bwd_supported(const AttnArgs &a);
+size_t fused_bwd_ws_bytes(int64_t bh, int L, int n);
+spion_status launch_bwd_fused(const AttnArgs &a, void *fws, cudaStream_t s);
+
 // a TMA tensor map (CUtensorMap, 128-byte aligned) over [bh][L][64] bf16, 128B swizzle; attn_tc.cu
 bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_bh, int64_t stride_l, int box_rows);
 

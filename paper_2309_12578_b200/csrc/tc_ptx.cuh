@@ -128,6 +128,14 @@ __device__ __forceinline__ void tma_store_3d(const void *tmap, const void *src, 
                  "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+// 3-D tiled reduce-add shared -> global (element type of the tensor map, performed at L2; bulk
+// async-group of the issuing thread)
+__device__ __forceinline__ void tma_reduce_add_3d(const void *tmap, const void *src, int c0, int c1, int c2) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until every committed bulk store of this thread has finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -232,6 +240,8 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // ------------------------------------------------------------------ descriptors
 // SWIZZLE_128B operand tile: rows of 128 bytes (64 bf16), 8-row atoms of 1024 B,
 // consecutive atoms along the strided dimension at SBO = 1024 B.
+// (MN-major SW128 operands: LBO = byte distance between consecutive 64-element MN chunks, SBO = between
+// consecutive 8-row K groups; K-major: SBO between 8-row MN groups, LBO unused)
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes = 16, uint32_t sbo_bytes = 1024) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -260,6 +270,36 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+
+// 1-D bulk reduction shared -> global (fp32 add, performed at L2), bulk async-group of the issuing
+// thread; 16-byte aligned addresses, size a multiple of 16
+__device__ __forceinline__ void bulk_reduce_add_f32(float *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                     reinterpret_cast<uint64_t>(gdst)),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+// wait until all but the N most recent committed bulk groups of this thread are complete / have read
+// their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// async-proxy global writes (bulk reductions) <-> generic-proxy accesses of this thread
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// drop a 128-byte L2 line without writing it back (its contents become indeterminate)
+__device__ __forceinline__ void discard_l2_line(const void *gaddr) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(gaddr)) : "memory");
+}
+// per-warpgroup register budget (all four warps of the warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
 // vector fp32 reduction into global memory (sm_90+)
 __device__ __forceinline__ void red_add_v4(float *gaddr, float a, float b, float c, float d) {

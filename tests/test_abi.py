@@ -118,7 +118,12 @@ def test_attn_path_query():
     assert lib.spion_attn_path(128, 4096, 64, 4096 * 64, 64, N.BF16, ctypes.byref(t)) in (N.PATH_CUDA_CORE,
                                                                                          N.PATH_TCGEN05)
     assert lib.spion_attn_fwd_workspace_bytes(128, 4096, 64, N.BF16) == 256
-    assert lib.spion_attn_workspace_bytes(128, 4096, 64, N.BF16) == 256 + 2 * 128 * 4096 * 4
+    # counters + D + -lse*log2e; for bf16 d=64 also the fused backward's completion counters (sized for
+    # block 32) and fp32 dQ accumulator [bh][L][64]
+    base = 256 + 2 * 128 * 4096 * 4
+    assert lib.spion_attn_workspace_bytes(128, 4096, 32, N.BF16) == base
+    assert lib.spion_attn_workspace_bytes(128, 4096, 64, N.F32) == base
+    assert lib.spion_attn_workspace_bytes(128, 4096, 64, N.BF16) == base + 128 * 128 * 4 + 128 * 4096 * 64 * 4
 
 
 def test_transition_rejects_bad_arguments():
