@@ -212,22 +212,26 @@ SPION_API spion_status spion_attn_fwd(const void *Q_dev, const void *K_dev, cons
  * through Z).  O and lse are the outputs of spion_attn_fwd.  dQ, dK, dV use
  * the same layout and strides as Q.  ws_dev: >= spion_attn_workspace_bytes
  * (see above).
- * Tensor-core path: block 64 runs ONE fused pass over the pattern's column
- * tiles (dK, dV accumulated per tile; dQ accumulated in fp32 in the
- * workspace by bulk reduce-adds at L2, so its summation order depends on
- * scheduling: dQ may differ between runs by rounding); block 32 (and block
- * 64 with SPION_BWD_DETERMINISTIC) runs a row pass for dQ and a column pass
- * for dK/dV, atomic-free and bitwise reproducible. */
+ * Tensor-core path: a row pass for dQ and a column pass for dK/dV,
+ * atomic-free and bitwise reproducible; block 64 can instead run ONE fused
+ * pass (spion_attn_bwd_ex, SPION_BWD_FUSED). */
 SPION_API spion_status spion_attn_bwd(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
                             const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev,
                             void *dV_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,
                             int64_t stride_l, spion_dtype dt, const spion_bsr *pat, spion_softmax_mode mode,
                             float scale, void *ws_dev, size_t ws_bytes, void *stream);
 
-/* spion_attn_bwd with flags (bitwise OR; other bits: SPION_ERR_PARAM):
+/* spion_attn_bwd with flags (bitwise OR; other bits, or both bits: SPION_ERR_PARAM):
  * SPION_BWD_DETERMINISTIC — bitwise reproducible results (the two-pass
- * tensor-core backward at every block size). */
-typedef enum { SPION_BWD_DETERMINISTIC = 1 } spion_bwd_flags;
+ *   tensor-core backward; also the default).
+ * SPION_BWD_FUSED — block 64 on the tensor-core path: one pass over the
+ *   pattern's column tiles computes dK, dV and dQ (dQ = [dS_I0; dS_I1] K per
+ *   pair of query blocks, accumulated in fp32 in the workspace by bulk
+ *   reduce-adds at L2 and converted by the last contributor), so Q, K, V and
+ *   dO are read and S^T, dP^T recomputed once; dQ's summation order depends on
+ *   scheduling (results may differ between runs by rounding).  Other shapes
+ *   ignore the flag. */
+typedef enum { SPION_BWD_DETERMINISTIC = 1, SPION_BWD_FUSED = 2 } spion_bwd_flags;
 SPION_API spion_status spion_attn_bwd_ex(const void *Q_dev, const void *K_dev, const void *V_dev, const void *O_dev,
                             const void *dO_dev, const float *lse_dev, void *dQ_dev, void *dK_dev,
                             void *dV_dev, int64_t bh, int32_t L, int32_t d, int64_t stride_bh,

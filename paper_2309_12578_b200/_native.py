@@ -12,7 +12,7 @@ OK = 0
 STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace", 6: "cuda", 7: "unsupported"}
 F32, BF16 = 0, 1
 PATH_CUDA_CORE, PATH_TCGEN05 = 0, 1  # spion_attn_path
-BWD_DETERMINISTIC = 1  # spion_attn_bwd_ex flags
+BWD_DETERMINISTIC, BWD_FUSED = 1, 2  # spion_attn_bwd_ex flags
 SOFTMAX = {"paper": 0, "masked": 1}
 THRESH = {"linear": 0, "nearest": 1, "absolute": 2}
 # spion_pattern_flags (include/spion.h): SPION-C, prose recursion, all-cells seeding
@@ -99,6 +99,8 @@ def lib():
             raise ImportError(f"libspion.so not found at {SO_PATH}; run __graft_entry__.build()")
         L = ctypes.CDLL(SO_PATH)
         for name, (res, args) in EXPORTS.items():
+            if os.environ.get("SPION_LIB") and not hasattr(L, name):
+                continue  # an older A/B build may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -221,9 +221,9 @@ size_t spion_attn_workspace_bytes(int64_t bh, int32_t L, int32_t d, spion_dtype 
     return b;
 }
 
-// SPION_SPLIT_BWD=1: the two-kernel (dQ row pass + dK/dV column pass) backward at B = 64 too
-static bool split_bwd_forced() {
-    static const int v = getenv("SPION_SPLIT_BWD") != nullptr;
+// SPION_FUSED_BWD=1: the fused single-pass backward at B = 64 without the flag (A/B timing)
+static bool fused_bwd_forced() {
+    static const int v = getenv("SPION_FUSED_BWD") != nullptr;
     return v != 0;
 }
 
@@ -322,7 +322,8 @@ spion_status spion_attn_bwd_ex(const void *Q_dev, const void *K_dev, const void 
                                int64_t bh, int32_t L, int32_t d, int64_t stride_bh, int64_t stride_l, spion_dtype dt,
                                const spion_bsr *pat, spion_softmax_mode mode, float scale, uint32_t flags,
                                void *ws_dev, size_t ws_bytes, void *stream) {
-    if (flags & ~(uint32_t)SPION_BWD_DETERMINISTIC) return SPION_ERR_PARAM;
+    if (flags & ~(uint32_t)(SPION_BWD_DETERMINISTIC | SPION_BWD_FUSED)) return SPION_ERR_PARAM;
+    if ((flags & SPION_BWD_DETERMINISTIC) && (flags & SPION_BWD_FUSED)) return SPION_ERR_PARAM;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     spion_status st = check_attn_common(Q_dev, K_dev, V_dev, bh, L, d, stride_bh, stride_l, dt, pat, mode);
     if (st) return st;
@@ -347,7 +348,8 @@ spion_status spion_attn_bwd_ex(const void *Q_dev, const void *K_dev, const void 
     if (path < 0) return (spion_status)(-path);
     if (path == SPION_PATH_TCGEN05) {
         SPION_CUDA_TRY(cudaMemsetAsync(ws_dev, 0, ATTN_CTR_BYTES, s));
-        if (fused_bwd_supported(a) && !split_bwd_forced() && !(flags & SPION_BWD_DETERMINISTIC))
+        const bool fused = (flags & SPION_BWD_FUSED) || (fused_bwd_forced() && !(flags & SPION_BWD_DETERMINISTIC));
+        if (fused && fused_bwd_supported(a))
             return launch_bwd_fused(a, static_cast<char *>(ws_dev) + attn_ws_base(bh, L), s);
         return launch_bwd_tc(a, s);
     }

@@ -30,6 +30,18 @@
 // accumulators [384,448) [448,512).
 #include "attn_tc.cuh"
 
+// timing-only debug builds (wrong dQ): no completion counting / finalisation; no dQ staging or
+// reduce-adds; no dQ MMA
+#ifndef SPION_FDBG_NOFIN
+#define SPION_FDBG_NOFIN 0
+#endif
+#ifndef SPION_FDBG_NODQ
+#define SPION_FDBG_NODQ 0
+#endif
+#ifndef SPION_FDBG_NODQMMA
+#define SPION_FDBG_NODQMMA 0
+#endif
+
 namespace spion {
 
 namespace {
@@ -282,7 +294,8 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
                             const uint64_t dS0 = sdesc_sw128(smem_u32(sDS + (gp & 1) * F_DSP), F_DSP / 2, 1024);
 #pragma unroll
                             for (int k = 0; k < 8; ++k)
-                                MMA_SS(tmem + COL_DQ + (gp & 1) * 64, dS0 + 128 * k, dKmn + 128 * k, IDESC_DQ, k > 0);
+                                if (!SPION_FDBG_NODQMMA)
+                                    MMA_SS(tmem + COL_DQ + (gp & 1) * 64, dS0 + 128 * k, dKmn + 128 * k, IDESC_DQ, k > 0);
                             mma_commit(dq_full + (gp & 1));
                         }
                         if (pj == cnt - 1) mma_commit(acc_full);
@@ -338,7 +351,7 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
         auto count_completed = [&](int nent, int bh, int I0, int I1) {
             // leader: the previous pair's reductions are complete (bulk_wait<1> / <0>); count them
             int nf = 0;
-            if (nent) {
+            if (nent && !SPION_FDBG_NOFIN) {
                 fence_proxy_async_global();
                 __threadfence();
                 if (atomicAdd(f.done + (int64_t)bh * p.n + I0, 1) == expc[I0] - 1) {
@@ -395,7 +408,7 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
                 mbar_arrive(dq_empty + acc);
                 // the dQ MMA has completed, so the pair's dS buffer is free: stage fp32 rows there
                 // ([64 queries][64] per entry, 256 B rows; chunk order rotated by row: conflict-free)
-                if (half == 0 || paired) {
+                if ((half == 0 || paired) && !SPION_FDBG_NODQ) {
                     // two [64 rows][32 fp32] TMA boxes per entry, 128-byte swizzled (the reduce's tensor
                     // map unswizzles): 16-byte chunk c of row qr at (c ^ (qr & 7)) -> conflict-free STS
                     uint8_t *dst = slot + half * (F_DSP / 2) + qr * 128;
@@ -409,7 +422,8 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
                 }
                 fence_proxy_async_smem();
                 named_bar_sync(BAR_DQ, 128);
-                if (leader) {
+                if (leader && SPION_FDBG_NODQ) mbar_arrive(ds_empty + acc);
+                if (leader && !SPION_FDBG_NODQ) {
                     const int I0 = rows[pj], I1 = paired ? rows[pj + 1] : 0;
                     tma_reduce_add_3d(&tmAcc, slot, 0, I0 * FB, bh);
                     tma_reduce_add_3d(&tmAcc, slot + 8192, 32, I0 * FB, bh);

@@ -66,7 +66,10 @@ template <int B> struct Cfg {
     static constexpr int DQ_NST = B == 32 ? 3 : 8;             // K_J + V_J per stage
     static constexpr int DKV_CTAS = B == 32 ? SPION_DKV_CTAS32 : 1, DKV_COLS = 512 / DKV_CTAS;
     static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
-    static constexpr int DKV_NST = B == 32 ? SPION_DKV_NST32 : 9;  // Q_I + dO_I + lse_I + D_I per stage
+    static constexpr int DKV_NST = B == 32 ? SPION_DKV_NST32 : 7;  // Q_I + dO_I + lse_I + D_I per stage
+    // K/V (and dK/dV staging) buffers across items: three where one CTA owns the SM, so the next
+    // item's K/V can load while the previous item's dK/dV store still holds its buffer
+    static constexpr int DKV_KVB = DKV_CTAS == 1 ? 3 : 2;
     // softmax warps of the backward kernels: two warpgroups (each takes half of a block's
     // columns) where one CTA owns the SM, one warpgroup where two CTAs share it
     static constexpr int DQ_MW = DQ_CTAS == 1 ? 8 : 4, DKV_MW = DKV_CTAS == 1 ? 8 : 4;
@@ -135,41 +138,61 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     if (warp == W_PROD) {
         // ------------------------------------------------------------ scheduler + TMA producer
         if (lane == 0) { prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmO); }
-        int st = 0, nq = 0, pre = -2;  // pre: next item index, prefetched during this item
+        // The next item is fetched from the scheduler when the current one starts, and its Q tile
+        // is issued as soon as a Q buffer frees up (tested between the current item's K/V stages),
+        // so the S-MMA warp finds it resident when it moves on.
+        int st = 0, nq = 0;
         uint32_t ph = 0;
-        for (int ks = 0;; ++ks) {
-            const int item = sched_produce(sc, ks, p, nitems, true, pre);
-            pre = -2;
-            if (item < 0) break;
+        int pre = sched_prefetch(p);
+        int item = sched_produce(sc, 0, p, nitems, true, pre);
+        pre = sched_prefetch(p);
+        bool issued = false;
+        auto item_tile = [&](int ks, bool block) -> bool {  // Q of ring item ks (false: buffer busy)
             const int *h = sc.hdr + (ks & 3) * 8;
-            const int bh = h[1], t = h[2], cnt = h[3];
-            const int *col = sc.col + (ks & 3) * SCHED_CAP;
-            if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the TMA
-                const int qb = nq & 1;
-                if (nq >= 2) mbar_wait(q_empty + qb, ((nq >> 1) - 1) & 1);
-                if (elect_one()) {
-                    mbar_arrive_expect_tx(q_full + qb, 16384);
-                    tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
-                }
-                __syncwarp();
-                ++nq;
-                for (int j = 0; j < cnt; ++j) {
-                    if (j == (cnt > 2 ? cnt - 2 : 0)) pre = sched_prefetch(p);
-                    mbar_wait(kv_empty + st, ph ^ 1);
-                    if (elect_one()) {
-                        if (SPION_DBG_NOLOAD) {
-                            mbar_arrive(kv_full + st);
-                        } else {
-                            mbar_arrive_expect_tx(kv_full + st, STG);
-                            tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                            tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
-                        }
-                    }
-                    __syncwarp();
-                    if (++st == NST) { st = 0; ph ^= 1; }
-                }
+            if (h[3] == 0) return true;
+            const int qb = nq & 1;
+            if (nq >= 2) {
+                const uint32_t par = ((nq >> 1) - 1) & 1;
+                if (block) mbar_wait(q_empty + qb, par);
+                else if (!warp_test(q_empty + qb, par)) return false;
+            }
+            if (elect_one()) {
+                mbar_arrive_expect_tx(q_full + qb, 16384);
+                tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, h[2] * 128, h[1]);
             }
             __syncwarp();
+            ++nq;
+            return true;
+        };
+        for (int ks = 0; item >= 0; ++ks) {
+            if (!issued) item_tile(ks, true);
+            // the next item: list loads issued now, stored after two of this item's stages
+            const SchedFetch nf = sched_fetch_begin(sc, ks + 1, p, nitems, pre);
+            pre = sched_prefetch(p);
+            const int nitem = nf.item;
+            bool ended = false, nissued = nitem < 0;
+            const int *h = sc.hdr + (ks & 3) * 8;
+            const int bh = h[1], cnt = h[3];
+            const int *col = sc.col + (ks & 3) * SCHED_CAP;
+            for (int j = 0; j < cnt; ++j) {  // whole warp runs the loop; one elected lane issues the TMA
+                if (!ended && j == 2) { sched_fetch_end(sc, ks + 1, p, nf, true); ended = true; }
+                if (ended && !nissued) nissued = item_tile(ks + 1, false);
+                mbar_wait(kv_empty + st, ph ^ 1);
+                if (elect_one()) {
+                    if (SPION_DBG_NOLOAD) {
+                        mbar_arrive(kv_full + st);
+                    } else {
+                        mbar_arrive_expect_tx(kv_full + st, STG);
+                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    }
+                }
+                __syncwarp();
+                if (++st == NST) { st = 0; ph ^= 1; }
+            }
+            if (!ended) sched_fetch_end(sc, ks + 1, p, nf, true);
+            issued = nissued;
+            item = nitem;
         }
     } else if (warp == W_MMA) {
         // ------------------------------------------------------------ S issuer (converged warp,
@@ -467,48 +490,75 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             prefetch_tmap(&tmQ); prefetch_tmap(&tmdO); prefetch_tmap(&tmO);
             prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmdQ);
         }
-        int st = 0, nq = 0, pre = -2;  // pre: next item index, prefetched during this item
+        // next item fetched at the start of the current one; its Q/dO and O tiles issued as soon as
+        // their buffers free up (tested between the current item's K/V stages)
+        int st = 0, nq = 0;
         uint32_t ph = 0;
-        for (int ks = 0;; ++ks) {
-            const int item = sched_produce(sc, ks, p, nitems, false, pre);
-            pre = -2;
-            if (item < 0) break;
+        int pre = sched_prefetch(p);
+        int item = sched_produce(sc, 0, p, nitems, false, pre);
+        pre = sched_prefetch(p);
+        int tstate = 0;  // per-item tiles of the item being prepared: 1 = Q/dO issued, 2 = O too
+        auto item_tile = [&](int ks, bool block) -> bool {
             const int *h = sc.hdr + (ks & 3) * 8;
-            const int bh = h[1], t = h[2], cnt = h[3];
-            const int *col = sc.col + (ks & 3) * SCHED_CAP;
-            if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the TMA
-                const int qb = nq & 1;
-                if (nq >= 2) mbar_wait(q_empty + qb, ((nq >> 1) - 1) & 1);
+            if (h[3] == 0) return true;
+            const int bh = h[1], t = h[2], qb = nq & 1;
+            if (tstate == 0) {
+                if (nq >= 2) {
+                    const uint32_t par = ((nq >> 1) - 1) & 1;
+                    if (block) mbar_wait(q_empty + qb, par);
+                    else if (!warp_test(q_empty + qb, par)) return false;
+                }
                 if (elect_one()) {
                     mbar_arrive_expect_tx(q_full + qb, 32768);
                     tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
                     tma_load_3d(sdO + qb * 16384, &tmdO, q_full + qb, 0, t * 128, bh);
                 }
                 __syncwarp();
-                if (nq >= 1) mbar_wait(o_empty, (nq - 1) & 1);
-                if (elect_one()) {
-                    mbar_arrive_expect_tx(o_full, 16384);
-                    tma_load_3d(sO, &tmO, o_full, 0, t * 128, bh);
-                }
-                __syncwarp();
-                ++nq;
-                for (int j = 0; j < cnt; ++j) {
-                    if (j == (cnt > 2 ? cnt - 2 : 0)) pre = sched_prefetch(p);
-                    mbar_wait(kv_empty + st, ph ^ 1);
-                    if (elect_one()) {
-                        if (SPION_DBG_NOLOAD) {
-                            mbar_arrive(kv_full + st);
-                        } else {
-                            mbar_arrive_expect_tx(kv_full + st, STG);
-                            tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                            tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
-                        }
-                    }
-                    __syncwarp();
-                    if (++st == NST) { st = 0; ph ^= 1; }
-                }
+                tstate = 1;
+            }
+            if (nq >= 1) {
+                if (block) mbar_wait(o_empty, (nq - 1) & 1);
+                else if (!warp_test(o_empty, (nq - 1) & 1)) return false;
+            }
+            if (elect_one()) {
+                mbar_arrive_expect_tx(o_full, 16384);
+                tma_load_3d(sO, &tmO, o_full, 0, t * 128, bh);
             }
             __syncwarp();
+            tstate = 0;
+            ++nq;
+            return true;
+        };
+        bool issued = false;
+        for (int ks = 0; item >= 0; ++ks) {
+            if (!issued) item_tile(ks, true);
+            // the next item: list loads issued now, stored after two of this item's stages
+            const SchedFetch nf = sched_fetch_begin(sc, ks + 1, p, nitems, pre);
+            pre = sched_prefetch(p);
+            const int nitem = nf.item;
+            bool ended = false, nissued = nitem < 0;
+            const int *h = sc.hdr + (ks & 3) * 8;
+            const int bh = h[1], cnt = h[3];
+            const int *col = sc.col + (ks & 3) * SCHED_CAP;
+            for (int j = 0; j < cnt; ++j) {  // whole warp runs the loop; one elected lane issues the TMA
+                if (!ended && j == 2) { sched_fetch_end(sc, ks + 1, p, nf, false); ended = true; }
+                if (ended && !nissued) nissued = item_tile(ks + 1, false);
+                mbar_wait(kv_empty + st, ph ^ 1);
+                if (elect_one()) {
+                    if (SPION_DBG_NOLOAD) {
+                        mbar_arrive(kv_full + st);
+                    } else {
+                        mbar_arrive_expect_tx(kv_full + st, STG);
+                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
+                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                    }
+                }
+                __syncwarp();
+                if (++st == NST) { st = 0; ph ^= 1; }
+            }
+            if (!ended) sched_fetch_end(sc, ks + 1, p, nf, false);
+            issued = nissued;
+            item = nitem;
         }
     } else if (warp == W_MMA || warp >= W_MMA3) {
         // S / dP issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
@@ -636,7 +686,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 continue;
             }
             const int qb = nq & 1;
-            const float nl2 = valid ? -p.lse[(int64_t)bh * p.L + row] * LOG2E : 0.f;
+            const float nl2 = valid ? -__ldcg(p.lse + (int64_t)bh * p.L + row) * LOG2E : 0.f;
             // D_i = dO_i . O_i from the staged (swizzled) tiles
             mbar_wait(q_full + qb, (nq >> 1) & 1);
             mbar_wait(o_full, nq & 1);
@@ -657,6 +707,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                     }
                 }
             }
+            // the release must follow the LAST shared-memory load of O / dO: an mbarrier arrive does not
+            // wait for outstanding LDS (ptxas issued it right behind them), so the producer could see it,
+            // TMA the next item's O over the tile and corrupt rows still being read.  The proxy fence
+            // (generic reads before the async-proxy TMA writes that follow the release) waits for them.
+            fence_proxy_async_smem();
             mbar_arrive(o_empty);
             if (valid && wg == 0) {
                 p.D[(int64_t)bh * p.L + row] = Dr;
@@ -741,6 +796,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcParams p) {
     constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF, MW = Cfg<B>::DKV_MW, NSW = Cfg<B>::DKV_NSW;
+    constexpr int KVB = Cfg<B>::DKV_KVB;
     constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
     constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
     constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
@@ -754,28 +810,28 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sKV = smem;  // buffer kb: K at kb*32768, V at kb*32768 + 16384
-    uint8_t *sStage = smem + 65536;
+    uint8_t *sStage = smem + KVB * 32768;
     uint8_t *sSched = sStage + NST * STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *kv_full = bars + 0, *kv_empty = bars + 2, *acc_full = bars + 4, *s_full = bars + 5,
+    uint64_t *kv_full = bars + 0, *kv_empty = bars + 3, *acc_full = bars + 6, *s_full = bars + 7,
              *p_full = s_full + 2 * NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
     Sched sc = make_sched(sSched, q_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
-    uint64_t *staged = q_empty + NST + 9;  // [2]: dK/dV of the item using K/V buffer kb staged there
-    uint64_t *acc_empty = staged + 2;      // the epilogue has read the dK/dV accumulators
+    uint64_t *staged = q_empty + NST + 9;  // [KVB]: dK/dV of the item using K/V buffer kb staged there
+    uint64_t *acc_empty = staged + 3;      // the epilogue has read the dK/dV accumulators
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         // kv_empty: the last S^T/dP^T MMA of the item, and the epilogue's TMA store of dK/dV
         // (staged in the same buffer) having read shared memory
-        for (int i = 0; i < 2; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, NSW + 1); }
+        for (int i = 0; i < KVB; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, NSW + 1); }
         // s_full[2b + w]: S^T, dP^T of buffer b ready for softmax warpgroup w (PP) — one barrier
         // per (buffer, consumer), so each has one in-order producer and one in-order consumer
         for (int i = 0; i < 2 * NBUF; ++i) mbar_init(s_full + i, 1);
         for (int i = 0; i < NBUF; ++i) { mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
         mbar_init(acc_full, 1);
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
+        for (int i = 0; i < KVB; ++i) mbar_init(staged + i, 32 * MW);
         mbar_init(acc_empty, 32 * MW);
         sched_init(sc, 2 + NSW + MW);
         fence_barrier_init();
@@ -795,59 +851,78 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmQ); prefetch_tmap(&tmdO);
             prefetch_tmap(&tmdK); prefetch_tmap(&tmdV);
         }
-        int st = 0, nk = 0, pre = -2;  // pre: next item index, prefetched during this item
+        // next item fetched at the start of the current one; its K/V tiles issued as soon as their
+        // buffer frees up (tested between the current item's Q/dO stages)
+        int st = 0, nk = 0;
         uint32_t ph = 0;
-        for (int ks = 0;; ++ks) {
-            const int item = sched_produce(sc, ks, p, nitems, false, pre);
-            pre = -2;
-            if (item < 0) break;
-            if (lane == 0) tr.ev(1);
+        int pre = sched_prefetch(p);
+        int item = sched_produce(sc, 0, p, nitems, false, pre, &tr);
+        pre = sched_prefetch(p);
+        auto item_tile = [&](int ks, bool block) -> bool {  // K/V of ring item ks (false: buffer busy)
             const int *h = sc.hdr + (ks & 3) * 8;
-            const int bh = h[1], t = h[2], cnt = h[3];
-            const int *rows = sc.col + (ks & 3) * SCHED_CAP;
-            if (cnt > 0) {  // whole warp runs the loop; one elected lane issues the copies
-                const int kb = nk & 1;
-                if (nk >= 2) mbar_wait(kv_empty + kb, ((nk >> 1) - 1) & 1);
-                if (lane == 0) tr.ev(2);
-                if (elect_one()) {
-                    // the tile's S block columns (plan bperm: heavy columns grouped), one B-row box
-                    // each at slot offset s*B rows (same SW128 layout as one 128-row box); empty
-                    // slots are not loaded (their rows are masked in every entry, never stored)
-                    const int *pm = sc.tab + TAB_PERM + t * p.S;
-                    int nval = 0;
-                    for (int sl = 0; sl < p.S; ++sl) nval += pm[sl] < p.n;
-                    mbar_arrive_expect_tx(kv_full + kb, (uint32_t)nval * 2 * B * 128);
-                    for (int sl = 0; sl < p.S; ++sl) {
-                        const int c = pm[sl];
-                        if (c >= p.n) continue;
-                        tma_load_3d(sKV + kb * 32768 + sl * B * 128, &tmK, kv_full + kb, 0, c * B, bh);
-                        tma_load_3d(sKV + kb * 32768 + 16384 + sl * B * 128, &tmV, kv_full + kb, 0, c * B, bh);
-                    }
-                }
-                __syncwarp();
-                ++nk;
-                for (int j = 0; j < cnt; ++j) {
-                    const int I = rows[j];
-                    if (j == (cnt > 2 ? cnt - 2 : 0)) pre = sched_prefetch(p);
-                    mbar_wait(q_empty + st, ph ^ 1);
-                    if (lane == 0) tr.ev(3);
-                    uint8_t *stg = sStage + st * STAGE;
-                    if (elect_one()) {
-                        if (SPION_DBG_NOLOAD) {
-                            mbar_arrive(q_full + st);
-                        } else {
-                            mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
-                            tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
-                            tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
-                            bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
-                            bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
-                        }
-                    }
-                    __syncwarp();
-                    if (++st == NST) { st = 0; ph ^= 1; }
+            if (h[3] == 0) return true;
+            const int bh = h[1], t = h[2], kb = nk % KVB;
+            if (nk >= KVB) {
+                const uint32_t par = ((nk / KVB) - 1) & 1;
+                if (block) mbar_wait(kv_empty + kb, par);
+                else if (!warp_test(kv_empty + kb, par)) return false;
+            }
+            if (lane == 0) tr.ev(2);
+            if (elect_one()) {
+                // the tile's S block columns (plan bperm: heavy columns grouped), one B-row box
+                // each at slot offset s*B rows (same SW128 layout as one 128-row box); empty
+                // slots are not loaded (their rows are masked in every entry, never stored)
+                const int *pm = sc.tab + TAB_PERM + t * p.S;
+                int nval = 0;
+                for (int sl = 0; sl < p.S; ++sl) nval += pm[sl] < p.n;
+                mbar_arrive_expect_tx(kv_full + kb, (uint32_t)nval * 2 * B * 128);
+                for (int sl = 0; sl < p.S; ++sl) {
+                    const int c = pm[sl];
+                    if (c >= p.n) continue;
+                    tma_load_3d(sKV + kb * 32768 + sl * B * 128, &tmK, kv_full + kb, 0, c * B, bh);
+                    tma_load_3d(sKV + kb * 32768 + 16384 + sl * B * 128, &tmV, kv_full + kb, 0, c * B, bh);
                 }
             }
             __syncwarp();
+            ++nk;
+            return true;
+        };
+        bool issued = false;
+        for (int ks = 0; item >= 0; ++ks) {
+            if (lane == 0) tr.ev(1);
+            if (!issued) item_tile(ks, true);
+            // the next item: list loads issued now, stored after two of this item's stages
+            const SchedFetch nf = sched_fetch_begin(sc, ks + 1, p, nitems, pre, &tr);
+            pre = sched_prefetch(p);
+            const int nitem = nf.item;
+            bool ended = false, nissued = nitem < 0;
+            const int *h = sc.hdr + (ks & 3) * 8;
+            const int bh = h[1], cnt = h[3];
+            const int *rows = sc.col + (ks & 3) * SCHED_CAP;
+            for (int j = 0; j < cnt; ++j) {  // whole warp runs the loop; one elected lane issues the copies
+                if (!ended && j == 2) { sched_fetch_end(sc, ks + 1, p, nf, false, &tr); ended = true; }
+                if (ended && !nissued) nissued = item_tile(ks + 1, false);
+                const int I = rows[j];
+                mbar_wait(q_empty + st, ph ^ 1);
+                if (lane == 0) tr.ev(3);
+                uint8_t *stg = sStage + st * STAGE;
+                if (elect_one()) {
+                    if (SPION_DBG_NOLOAD) {
+                        mbar_arrive(q_full + st);
+                    } else {
+                        mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
+                        tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
+                        tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
+                        bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                        bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
+                    }
+                }
+                __syncwarp();
+                if (++st == NST) { st = 0; ph ^= 1; }
+            }
+            if (!ended) sched_fetch_end(sc, ks + 1, p, nf, false, &tr);
+            issued = nissued;
+            item = nitem;
         }
     } else if (warp == W_MMA || warp >= W_MMA3) {
         // S^T / dP^T issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
@@ -862,8 +937,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             if (lane == 0) tr.ev(10);
             const int cnt = h[3];
             if (cnt > 0) {
-                const int kb = nk & 1;
-                mbar_wait(kv_full + kb, (nk >> 1) & 1);
+                const int kb = nk % KVB;
+                mbar_wait(kv_full + kb, (nk / KVB) & 1);
                 if (lane == 0) tr.ev(11);
                 tc_fence_after();
                 ++nk;
@@ -963,8 +1038,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             if (h[0] < 0) break;
             const int bh = h[1], t = h[2], cnt = h[3];
             if (cnt > 0) {
-                const int sb = ns & 1;
-                mbar_wait(staged + sb, (ns >> 1) & 1);
+                const int sb = ns % KVB;
+                mbar_wait(staged + sb, (ns / KVB) & 1);
                 ++ns;
                 if (lane == 0) {
                     const int *pm = sc.tab + TAB_PERM + t * p.S;
@@ -1079,7 +1154,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             tc_fence_after();
             // dK, dV -> bf16 staged in this item's K/V buffer (free: every S^T/dP^T MMA is done),
             // then one TMA store per tile (coalesced; rows past L clipped)
-            const int kb = nk & 1;
+            const int kb = nk % KVB;
             ++nk;
             uint8_t *sdK = sKV + kb * 32768, *sdV = sdK + 16384;
             if (MW == 8) {  // warpgroup 0 stages dK, warpgroup 1 stages dV
@@ -1250,7 +1325,9 @@ TcParams tc_base_params(const AttnArgs &a, int which, int ctas, int gmult) {
 
 template <int B> static size_t fwd_smem() { return 1024 + 32768 + Cfg<B>::FWD_NST * 2 * B * 128 + SCHED_AREA; }
 template <int B> static size_t dq_smem() { return 1024 + 81920 + Cfg<B>::DQ_NST * 2 * B * 128 + SCHED_AREA; }
-template <int B> static size_t dkv_smem() { return 1024 + 65536 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + SCHED_AREA; }
+template <int B> static size_t dkv_smem() {
+    return 1024 + Cfg<B>::DKV_KVB * 32768 + Cfg<B>::DKV_NST * (2 * B * 128 + 1024) + SCHED_AREA;
+}
 
 static int grid_for(const TcParams &p, int ctas) {
     const int64_t items = p.bh * p.ntiles;

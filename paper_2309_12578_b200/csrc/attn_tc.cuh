@@ -172,58 +172,104 @@ __device__ __forceinline__ int sched_prefetch(const TcParams &p) {
     return (threadIdx.x & 31) == 0 ? atomicAdd(p.sched, 1) : 0;
 }
 
-// whole producer warp; returns the item (-1 = no more work).  pre: a prefetched item index
-// (sched_prefetch, valid in lane 0), or -2 to fetch one now
-__device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcParams &p, int nitems, bool want_rc,
-                                             int pre = -2) {
+// The producer fetches an item in two halves, so the global-memory round trips (the item
+// counter's atomic, prefetched with sched_prefetch, and the tile's entry lists) overlap its TMA
+// issue for the current item: sched_fetch_begin claims ring slot k and issues the list loads
+// into registers (lane e holds entries e, e+32, e+64, e+96; n <= SCHED_CAP = 128);
+// sched_fetch_end stores them to the slot and signals `full`.  Whole producer warp.
+struct SchedFetch {
+    int item, bh, t, cnt;
+    int col[4], msk[4];
+};
+
+__device__ __forceinline__ SchedFetch sched_fetch_begin(const Sched &sc, int k, const TcParams &p, int nitems,
+                                                        int pre, Tracer *tr = nullptr) {
     const int lane = threadIdx.x & 31;
     const int slot = k & 3;
+    SchedFetch f;
     mbar_wait(sc.empty + slot, ((k >> 2) & 1) ^ 1);
+    if (tr && lane == 0) tr->ev(5);
     int item = pre != -2 ? pre : sched_prefetch(p);
     item = __shfl_sync(0xffffffffu, item, 0);
+    f.item = item < nitems ? item : -1;
+    f.bh = f.t = f.cnt = 0;
+    if (f.item < 0) return f;
+    // chunks of G (batch, head), each chunk's tiles in descending work order (its K/V or
+    // Q/dO stay in L2), with the heavy tiles (> 2x the mean work) of chunk c+A handed out
+    // before the light tiles of chunk c (A = SPION_HEAVY_AHEAD): long tiles start A chunks
+    // early, so none is left for the end of the launch, while the L2 working set stays
+    // A + 1 chunks.  Block order (A = 1): H0, H1, L0, H2, L1, ..., H(C-1), L(C-2), L(C-1)
+    const int nh = sc.tab[0];
+    const int nbh = (int)p.bh, C = (nbh + p.G - 1) / p.G;
+    int rem = item, kk = 0, bh = 0;
+    auto take = [&](int c, bool heavy) {
+        const int Gc = min(p.G, nbh - c * p.G), sz = (heavy ? nh : p.ntiles - nh) * Gc;
+        if (rem < sz) {
+            const int k2 = rem / Gc;
+            bh = c * p.G + (rem - k2 * Gc);
+            kk = heavy ? k2 : nh + k2;
+            return true;
+        }
+        rem -= sz;
+        return false;
+    };
+    bool found = false;
+    for (int c = 0; c < min(SPION_HEAVY_AHEAD, C) && !found; ++c) found = take(c, true);
+    for (int c = 0; c < C && !found; ++c)
+        found = (c + SPION_HEAVY_AHEAD < C && take(c + SPION_HEAVY_AHEAD, true)) || take(c, false);
+    const int t = sc.tab[TAB_ORDER + kk];
+    const int beg = sc.tab[TAB_PTR + t], cnt = sc.tab[TAB_PTR + t + 1] - beg;
+    f.bh = bh;
+    f.t = t;
+    f.cnt = cnt;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int e = lane + 32 * i;
+        f.col[i] = e < cnt ? p.plan[p.off_col + beg + e] : 0;
+        f.msk[i] = e < cnt ? p.plan[p.off_msk + beg + e] : 0;
+    }
+    return f;
+}
+
+__device__ __forceinline__ void sched_fetch_end(const Sched &sc, int k, const TcParams &p, const SchedFetch &f,
+                                                bool want_rc, Tracer *tr = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int slot = k & 3;
     int *h = sc.hdr + slot * 8;
-    if (item >= nitems) {
-        item = -1;
+    if (f.item < 0) {
         if (lane == 0) h[0] = -1;
     } else {
-        // chunks of G (batch, head), each chunk's tiles in descending work order (its K/V or
-        // Q/dO stay in L2), with the heavy tiles (> 2x the mean work) of chunk c+A handed out
-        // before the light tiles of chunk c (A = SPION_HEAVY_AHEAD): long tiles start A chunks
-        // early, so none is left for the end of the launch, while the L2 working set stays
-        // A + 1 chunks.  Block order (A = 1): H0, H1, L0, H2, L1, ..., H(C-1), L(C-2), L(C-1)
-        const int nh = sc.tab[0];
-        const int nbh = (int)p.bh, C = (nbh + p.G - 1) / p.G;
-        int rem = item, kk = 0, bh = 0;
-        auto take = [&](int c, bool heavy) {
-            const int Gc = min(p.G, nbh - c * p.G), sz = (heavy ? nh : p.ntiles - nh) * Gc;
-            if (rem < sz) {
-                const int k2 = rem / Gc;
-                bh = c * p.G + (rem - k2 * Gc);
-                kk = heavy ? k2 : nh + k2;
-                return true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int e = lane + 32 * i;
+            if (e < f.cnt) {
+                sc.col[slot * SCHED_CAP + e] = f.col[i];
+                sc.msk[slot * SCHED_CAP + e] = f.msk[i];
             }
-            rem -= sz;
-            return false;
-        };
-        bool found = false;
-        for (int c = 0; c < min(SPION_HEAVY_AHEAD, C) && !found; ++c) found = take(c, true);
-        for (int c = 0; c < C && !found; ++c)
-            found = (c + SPION_HEAVY_AHEAD < C && take(c + SPION_HEAVY_AHEAD, true)) || take(c, false);
-        const int t = sc.tab[TAB_ORDER + kk];
-        const int beg = sc.tab[TAB_PTR + t], cnt = sc.tab[TAB_PTR + t + 1] - beg;
-        for (int e = lane; e < cnt; e += 32) {
-            sc.col[slot * SCHED_CAP + e] = p.plan[p.off_col + beg + e];
-            sc.msk[slot * SCHED_CAP + e] = p.plan[p.off_msk + beg + e];
         }
+        if (tr && lane == 0) tr->ev(6);
         if (want_rc && lane < 4) {
-            const int I = t * p.S + lane;
+            const int I = f.t * p.S + lane;
             h[4 + lane] = (lane < p.S && I < p.n) ? sc.tab[TAB_RC + I] : 0;
         }
-        if (lane == 0) { h[0] = item; h[1] = bh; h[2] = t; h[3] = cnt; }
+        if (lane == 0) { h[0] = f.item; h[1] = f.bh; h[2] = f.t; h[3] = f.cnt; }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(sc.full + slot);
-    return item;
+}
+
+// both halves at once; returns the item (-1 = no more work).  pre: a prefetched item index
+// (sched_prefetch, valid in lane 0), or -2 to fetch one now
+__device__ __forceinline__ int sched_produce(const Sched &sc, int k, const TcParams &p, int nitems, bool want_rc,
+                                             int pre = -2, Tracer *tr = nullptr) {
+    const SchedFetch f = sched_fetch_begin(sc, k, p, nitems, pre, tr);
+    sched_fetch_end(sc, k, p, f, want_rc, tr);
+    return f.item;
+}
+
+// non-blocking warp-uniform test of an mbarrier phase (lane 0's view, broadcast)
+__device__ __forceinline__ bool warp_test(uint64_t *bar, uint32_t parity) {
+    return __shfl_sync(0xffffffffu, (int)mbar_test(bar, parity), 0) != 0;
 }
 
 __device__ __forceinline__ const int *sched_wait(const Sched &sc, int k) {

@@ -267,6 +267,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
+// order point: the value must be computed (every load it depends on returned) before the next
+// memory / barrier instruction issues (an mbarrier arrive does not wait for outstanding loads)
+__device__ __forceinline__ void consume_reg(float x) { asm volatile("" ::"f"(x) : "memory"); }
+__device__ __forceinline__ void consume_reg(uint32_t x) { asm volatile("" ::"r"(x) : "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

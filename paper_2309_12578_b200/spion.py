@@ -206,10 +206,11 @@ def attn_workspace(bh: int, L: int, d: int, dtype, device) -> torch.Tensor:
 
 
 def attn_bwd(q, k, v, o, do, lse, bp: BlockPattern, mode: str = "paper", scale: Optional[float] = None,
-             workspace: Optional[torch.Tensor] = None, dq=None, dk=None, dv=None, deterministic: bool = False):
-    """dQ, dK, dV of block-sparse attention (reading Q17).  ``deterministic``: bitwise reproducible
-    (the two-pass tensor-core backward; by default block 64 runs the fused pass, whose dQ is summed
-    by L2 reduce-adds in scheduling order)."""
+             workspace: Optional[torch.Tensor] = None, dq=None, dk=None, dv=None, deterministic: bool = False,
+             fused: bool = False):
+    """dQ, dK, dV of block-sparse attention (reading Q17).  Default: the two-pass tensor-core backward
+    (bitwise reproducible; ``deterministic`` asks for it explicitly).  ``fused``: block 64 runs ONE
+    pass over the column tiles (dQ summed by L2 reduce-adds in scheduling order)."""
     _require_cuda(q, k, v, o, do, lse)
     bh, L, d, sb, sl = _layout(q)
     for t in (k, v, o, do):
@@ -224,10 +225,15 @@ def attn_bwd(q, k, v, o, do, lse, bp: BlockPattern, mode: str = "paper", scale: 
     dk = mk() if dk is None else dk
     dv = mk() if dv is None else dv
     s = bp.c_struct()
-    st = N.lib().spion_attn_bwd_ex(_p(q), _p(k), _p(v), _p(o), _p(do), _p(lse), _p(dq), _p(dk), _p(dv), bh, L, d,
-                                   sb, sl, _dtype_code(q), ctypes.byref(s), N.SOFTMAX[mode], float(scale),
-                                   N.BWD_DETERMINISTIC if deterministic else 0, _p(workspace), workspace.numel(),
-                                   _stream(q.device))
+    flags = (N.BWD_DETERMINISTIC if deterministic else 0) | (N.BWD_FUSED if fused else 0)
+    if flags:
+        st = N.lib().spion_attn_bwd_ex(_p(q), _p(k), _p(v), _p(o), _p(do), _p(lse), _p(dq), _p(dk), _p(dv), bh, L, d,
+                                       sb, sl, _dtype_code(q), ctypes.byref(s), N.SOFTMAX[mode], float(scale), flags,
+                                       _p(workspace), workspace.numel(), _stream(q.device))
+    else:
+        st = N.lib().spion_attn_bwd(_p(q), _p(k), _p(v), _p(o), _p(do), _p(lse), _p(dq), _p(dk), _p(dv), bh, L, d, sb,
+                                    sl, _dtype_code(q), ctypes.byref(s), N.SOFTMAX[mode], float(scale), _p(workspace),
+                                    workspace.numel(), _stream(q.device))
     N.check(st, "spion_attn_bwd")
     return dq, dk, dv
 

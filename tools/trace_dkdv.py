@@ -14,7 +14,7 @@ d = 64
 dev = torch.device("cuda:0")
 A = synth.lra_scores(L, B, seed=1, device=dev)
 q, k, v, do = synth.qkvdo(bh, L, d, seed=3, dtype=torch.bfloat16, device=dev)
-bp = spion.pattern(A, B, filter=31, alpha=75.0, sync=True)
+bp = spion.pattern(A, B, filter=31, alpha=float(os.environ.get("ALPHA", "55")), sync=True)
 o, lse = spion.attn_fwd(q, k, v, bp)
 for _ in range(3):
     spion.attn_bwd(q, k, v, o, do, lse, bp)
@@ -25,7 +25,7 @@ R = 5
 buf = (ctypes.c_ulonglong * (8 * 2048))()
 n = lib.spion_debug_trace(buf, 8 * 2048)
 a = np.array(buf[:n], dtype=np.uint64).reshape(8, 2048)
-names = {1: "P item", 2: "P KV issue", 3: "P Q issue", 10: "M item", 11: "M kv_full", 12: "S waits done",
+names = {1: "P item", 2: "P KV issue", 3: "P Q issue", 5: "P sched slot free", 6: "P lists loaded", 7: "P kv_empty done", 10: "M item", 11: "M kv_full", 12: "S waits done",
          13: "dVdK p_full done", 14: "S syncwarp done", 15: "dVdK syncwarp done", 20: "sm item", 21: "sm s_full",
          22: "sm p arrive", 23: "sm acc_full", 24: "sm epi done", 30: "dVdK loop top", 31: "dVdK elect",
          32: "dVdK MMAs issued", 33: "dVdK commits done", 40: "S loop top", 41: "S commits done", 42: "S q_full done",
@@ -59,3 +59,7 @@ print("dVdK issues", len(iss), "median gap", sorted(g for g, _ in gaps)[len(gaps
 print("largest gaps (cycles, at):", sorted(gaps, reverse=True)[:12])
 print("item starts:", [c - c0 for c in items][:40])
 print("first/last event of the CTA:", evs[0][0] - c0, evs[-1][0] - c0)
+if len(sys.argv) > 3:  # dump every event: cycle role name
+    with open(sys.argv[3], "w") as fo:
+        for c, e, r in evs:
+            fo.write(f"{c - c0} {r} {names.get(e, e)}\n")
