@@ -80,6 +80,7 @@ def config_dict(cfg, args, world):
         "workload": cfg["workload"], "L": cfg["L"], "block": cfg["block"], "heads": cfg["heads"], "d": cfg["d"],
         "batch": cfg["batch"], "towers": cfg["towers"], "bh": bh, "filter": FILTER, "alpha": args.alpha,
         "softmax": args.mode, "step": "pattern(scores)+attn_fwd+attn_bwd",
+        "pipeline": "sequential" if args.no_pipeline else "pattern of step i+1 on a second stream during step i's attention",
         "parallelism": f"dp{world} over batch*head ({args.scaling} scaling)",
         "l2": "rotating input sets, >= 2x L2 of other data between two uses of a set",
     }
@@ -338,6 +339,9 @@ def main():
     ap.add_argument("--mode", default="paper", choices=["paper", "masked"])
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of CUDA-graph replays")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="run each step's pattern on the attention stream (default: the next step's pattern "
+                         "runs on a second stream, concurrent with this step's attention)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="cpu_baseline leg: seconds of oracle work")
     ap.add_argument("--cpu-budget-total", type=float, default=120.0, help="--impl reference: seconds for the run")
@@ -353,8 +357,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args, cfg)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nRanks) for the record ...
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout keeps the one JSON line
 
     from paper_2309_12578_b200 import spion
     from paper_2309_12578_b200 import _native as N
@@ -414,23 +419,55 @@ def main():
         torch.cuda.synchronize()
         phases = [Phases(make_phases(i), not args.no_graphs, stream) for i in range(NSETS)]
 
+        # Pipelined steps (default): step i runs fwd + bwd of input set i on `stream` once pattern i is
+        # ready, and launches pattern i+1 (an independent input) on `pstream`, so the pattern kernels
+        # (the single-CTA finalize in particular) overlap this step's attention.  Every step still does
+        # the whole hot path: K timed steps contain exactly K patterns, K forwards and K backwards.
+        pstream = torch.cuda.Stream(dev)
+        pat_done = [torch.cuda.Event() for _ in range(NSETS)]
+        att_done = [torch.cuda.Event() for _ in range(NSETS)]
+        for e in att_done:
+            e.record(stream)
+
+        def pattern_on_pstream(j, ev=None):
+            pstream.wait_event(att_done[j])  # the last attention that read pattern buffer j is done
+            with torch.cuda.stream(pstream):
+                if ev is not None:
+                    ev[0].record(pstream)
+                phases[j].run(0)
+                if world > 1:
+                    broadcast_pattern(bps[j].flat, src=0)  # the per-layer pattern: one NCCL collective
+                if ev is not None:
+                    ev[1].record(pstream)
+                pat_done[j].record(pstream)
+
         def step(i, ev=None):
             j = i % NSETS
             ph = phases[j]
-            if ev is not None:
-                ev[0].record(stream)
-            ph.run(0)
-            if world > 1:
-                broadcast_pattern(bps[j].flat, src=0)  # the per-layer pattern: one NCCL collective
-            if ev is not None:
-                ev[1].record(stream)
-            ph.run(1)
+            if args.no_pipeline:
+                if ev is not None:
+                    ev[0].record(stream)
+                ph.run(0)
+                if world > 1:
+                    broadcast_pattern(bps[j].flat, src=0)  # the per-layer pattern: one NCCL collective
+                if ev is not None:
+                    ev[1].record(stream)
+            else:
+                stream.wait_event(pat_done[j])
             if ev is not None:
                 ev[2].record(stream)
-            ph.run(2)
+            ph.run(1)
             if ev is not None:
                 ev[3].record(stream)
+            ph.run(2)
+            if ev is not None:
+                ev[4].record(stream)
+            if not args.no_pipeline:
+                att_done[j].record(stream)
+                pattern_on_pstream((i + 1) % NSETS, ev[5:] if ev is not None else None)
 
+        if not args.no_pipeline:
+            pattern_on_pstream(0)
         for i in range(args.warmup):
             step(i)
         torch.cuda.synchronize()
@@ -439,14 +476,16 @@ def main():
     density = nnzb / (L // B) ** 2
 
     # ---- timed region: K steps; events on the launching stream at the phase boundaries
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream), ClockSampler(dev.index if dev.index is not None else 0) as clk:
         barrier(dist)
         torch.cuda.synchronize()
         start.record(stream)
-        for i in range(args.steps):
-            step(i, evs[i])
+        for i in range(args.warmup, args.warmup + args.steps):
+            step(i, evs[i - args.warmup])
+        if not args.no_pipeline:
+            stream.wait_event(pat_done[(args.warmup + args.steps) % NSETS])  # the K-th pattern of the region
         end.record(stream)
         torch.cuda.synchronize()
         barrier(dist)
@@ -458,9 +497,9 @@ def main():
         ms = float(t.item())
     ph = {"pattern": [], "fwd": [], "bwd": []}
     for e in evs:
-        ph["pattern"].append(e[0].elapsed_time(e[1]))
-        ph["fwd"].append(e[1].elapsed_time(e[2]))
-        ph["bwd"].append(e[2].elapsed_time(e[3]))
+        ph["pattern"].append(e[0].elapsed_time(e[1]) if args.no_pipeline else e[5].elapsed_time(e[6]))
+        ph["fwd"].append(e[2].elapsed_time(e[3]))
+        ph["bwd"].append(e[3].elapsed_time(e[4]))
     ph_ms = {k_: statistics.mean(v_) for k_, v_ in ph.items()}
 
     # ---- roofline of the dominant call (algorithmic bytes / measured duration)

@@ -41,6 +41,12 @@
 #ifndef SPION_FDBG_NODQMMA
 #define SPION_FDBG_NODQMMA 0
 #endif
+#ifndef SPION_FDBG_NODISCARD  // keep finalised fp32 lines in L2 (A/B of discard.global.L2)
+#define SPION_FDBG_NODISCARD 0
+#endif
+#ifndef SPION_FDBG_NOFINLOAD  // count completions but skip the finalisation loads / stores (timing)
+#define SPION_FDBG_NOFINLOAD 0
+#endif
 
 namespace spion {
 
@@ -132,7 +138,7 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
     Sched sc = make_sched(sSched, sched_bars);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sched_bars + 8);
     int *expc = reinterpret_cast<int *>(tmem_slot + 4);  // [n] contributions expected per query block
-    int *fin = expc + SCHED_CAP;                         // dQ warpgroup: [0] count, [1..] (bh, I) to finalise
+    int *fin = expc + SCHED_CAP;                         // dQ warpgroup: finalisation queue (2 + 2 * 64 ints)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -163,7 +169,7 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
     const uint32_t tmem = *tmem_slot;
     const int nitems = (int)(p.bh * p.ntiles);
     // register budgets per warpgroup (each warpgroup executes one setmaxnreg at the top of its branch):
-    // softmax 2 x 128 x 176 + dQ 128 x 96 + single-lane roles 128 x 56 = 64512 <= 65536
+    // softmax 2 x 128 x 168 + dQ 128 x 120 + single-lane roles 128 x 56 = 65536
     if (warp >= W_PROD) {
     regs_dec<56>();
     if (warp == W_PROD) {
@@ -339,56 +345,98 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
     }
     } else if (warp >= W_DQ0) {
         // ------------------------------------------------------------ dQ warpgroup
-        regs_dec<96>();
+        // Per pair: TMEM -> staged fp32 rows -> TMA reduce-adds (leader).  Completion bookkeeping is
+        // lagged so no global round trip blocks the pair loop: at pair p the leader waits for pair
+        // p-1's reductions (issued a pair ago), issues its two completion-counter atomics, and consumes
+        // the atomics issued at pair p-1 (for pair p-2): a query block whose count reached the plan's
+        // contribution count joins a shared-memory queue.  Finalising one queued block takes two
+        // pairs: its fp32 rows are loaded into registers at the end of one pair and converted /
+        // stored (and their L2 lines discarded) at the end of the next.
+        regs_dec<120>();
         const int q4 = warp & 3;
         const int row = q4 * 32 + lane;   // accumulator row = TMEM lane: pair half row / 64, query row % 64
         const int half = row >> 6, qr = row & 63;
+        const int tq = threadIdx.x - W_DQ0 * 32;  // 0..127: finalise row tq/2, 32-column half tq&1
         const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
         const bool leader = warp == W_DQ0 && lane == 0;
-        // the leader's record of the previous pair (completion counted one pair later)
-        int prev_n = 0, prev_bh = 0, prev_I0 = 0, prev_I1 = 0;
-        uint32_t gp = 0;
-        auto count_completed = [&](int nent, int bh, int I0, int I1) {
-            // leader: the previous pair's reductions are complete (bulk_wait<1> / <0>); count them
-            int nf = 0;
-            if (nent && !SPION_FDBG_NOFIN) {
-                fence_proxy_async_global();
-                __threadfence();
-                if (atomicAdd(f.done + (int64_t)bh * p.n + I0, 1) == expc[I0] - 1) {
-                    fin[1] = bh;
-                    fin[2] = I0;
-                    ++nf;
-                }
-                if (nent > 1 && atomicAdd(f.done + (int64_t)bh * p.n + I1, 1) == expc[I1] - 1) {
-                    fin[1 + 2 * nf] = bh;
-                    fin[2 + 2 * nf] = I1;
-                    ++nf;
-                }
-                if (nf) __threadfence();
-            }
-            fin[0] = nf;
+        int *fq = fin;              // [0] head (leader only), [1] tail, [2..] ring of FQ (bh, I)
+        constexpr int FQ = 64;
+        if (leader) { fq[0] = 0; fq[1] = 0; }
+        // leader state: the previous pair, awaiting completion (A); completed entries not yet counted
+        // (pending, shared memory); counter atomics issued, results not yet consumed (R, registers).
+        // The counting is batched: one release fence per batch of up to 8 entries.
+        int a_n = 0, a_bh = 0, a_I0 = 0, a_I1 = 0;
+        int *pend = fq + 2 + 2 * FQ;  // [8][2] (bh, I)
+        int np = 0, nr = 0;
+        int rr[8], rbh[8], rI[8];
+        auto push = [&](int bh, int I) {
+            const int t = fq[1];
+            fq[2 + 2 * (t % FQ)] = bh;
+            fq[3 + 2 * (t % FQ)] = I;
+            fq[1] = t + 1;
         };
-        auto finalize = [&]() {
-            // every dQ warpgroup thread: convert the finished query blocks (fp32 dQacc, L2) to bf16 dQ
-            const int nf = fin[0];
-            for (int e = 0; e < nf; ++e) {
-                const int bh = fin[1 + 2 * e], I = fin[2 + 2 * e];
-                const int t = threadIdx.x - W_DQ0 * 32;  // 0..127: row t/2, 32-column half t&1
-                const int r = t >> 1, hc = t & 1;
-                const float *src = f.dQacc + ((int64_t)bh * p.L + (int64_t)I * FB + r) * 64 + hc * 32;
-                float v[32];
+        auto consume_r = [&]() {  // leader: the batch of atomics issued before has returned
+            bool any = false;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float4 x = __ldcg(reinterpret_cast<const float4 *>(src) + c);
-                    v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
+            for (int i = 0; i < 8; ++i)
+                if (i < nr && rr[i] == expc[rI[i]] - 1) {
+                    push(rbh[i], rI[i]);
+                    any = true;
                 }
-                __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(f.dQ) + (int64_t)bh * p.stride_bh +
-                                     (int64_t)(I * FB + r) * p.stride_l;
-                store_row_bf16(dst, v, p.scale, hc);
-                // the 16 KB of fp32 rows are dead: drop them from L2 without a write-back
-                discard_l2_line(f.dQacc + ((int64_t)bh * p.L + (int64_t)I * FB) * 64 + t * 32);
+            if (any) __threadfence();  // acquire: the other contributors' reductions happen-before the loads
+            nr = 0;
+        };
+        auto flush = [&]() {  // leader: count every pending (completed) entry
+            consume_r();
+            if (np == 0) return;
+            fence_proxy_async_global();
+            __threadfence();  // release: this CTA's completed reductions before its counter increments
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < np) {
+                    rbh[i] = pend[2 * i];
+                    rI[i] = pend[2 * i + 1];
+                    rr[i] = atomicAdd(f.done + (int64_t)rbh[i] * p.n + rI[i], 1);
+                }
+            nr = np;
+            np = 0;
+        };
+        auto complete_a = [&]() {  // leader: pair A's reductions are complete -> pending
+            for (int e = 0; e < a_n; ++e) {
+                pend[2 * np] = a_bh;
+                pend[2 * np + 1] = e == 0 ? a_I0 : a_I1;
+                ++np;
+            }
+            a_n = 0;
+            if (np >= 6) flush();
+        };
+        // finaliser state (every thread): one block loaded in registers, waiting to be stored
+        int f_bh = -1, f_I = 0, f_head = 0;
+        float fv[32];
+        auto fin_store = [&]() {
+            if (f_bh < 0) return;
+            __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(f.dQ) + (int64_t)f_bh * p.stride_bh +
+                                 (int64_t)(f_I * FB + (tq >> 1)) * p.stride_l;
+            store_row_bf16(dst, fv, p.scale, tq & 1);
+            // the 16 KB of fp32 rows are dead: drop them from L2 without a write-back
+            if (!SPION_FDBG_NODISCARD) discard_l2_line(f.dQacc + ((int64_t)f_bh * p.L + (int64_t)f_I * FB) * 64 + tq * 32);
+            f_bh = -1;
+        };
+        auto fin_load = [&](int tail) {  // after a barrier: start the next queued block, if any
+            if (f_head >= tail) return;
+            if (SPION_FDBG_NOFINLOAD) { f_head = tail; return; }
+            f_bh = fq[2 + 2 * (f_head % FQ)];
+            f_I = fq[3 + 2 * (f_head % FQ)];
+            ++f_head;
+            const float4 *src = reinterpret_cast<const float4 *>(
+                f.dQacc + ((int64_t)f_bh * p.L + (int64_t)f_I * FB + (tq >> 1)) * 64 + (tq & 1) * 32);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float4 x = __ldcg(src + c);
+                fv[4 * c] = x.x; fv[4 * c + 1] = x.y; fv[4 * c + 2] = x.z; fv[4 * c + 3] = x.w;
             }
         };
+        uint32_t gp = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -406,8 +454,7 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
                 tmem_ld_wait();
                 tc_fence_before();
                 mbar_arrive(dq_empty + acc);
-                // the dQ MMA has completed, so the pair's dS buffer is free: stage fp32 rows there
-                // ([64 queries][64] per entry, 256 B rows; chunk order rotated by row: conflict-free)
+                // the dQ MMA has completed, so the pair's dS buffer is free: stage the fp32 rows there
                 if ((half == 0 || paired) && !SPION_FDBG_NODQ) {
                     // two [64 rows][32 fp32] TMA boxes per entry, 128-byte swizzled (the reduce's tensor
                     // map unswizzles): 16-byte chunk c of row qr at (c ^ (qr & 7)) -> conflict-free STS
@@ -422,40 +469,58 @@ attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_c
                 }
                 fence_proxy_async_smem();
                 named_bar_sync(BAR_DQ, 128);
-                if (leader && SPION_FDBG_NODQ) mbar_arrive(ds_empty + acc);
-                if (leader && !SPION_FDBG_NODQ) {
-                    const int I0 = rows[pj], I1 = paired ? rows[pj + 1] : 0;
-                    tma_reduce_add_3d(&tmAcc, slot, 0, I0 * FB, bh);
-                    tma_reduce_add_3d(&tmAcc, slot + 8192, 32, I0 * FB, bh);
-                    if (paired) {
-                        tma_reduce_add_3d(&tmAcc, slot + F_DSP / 2, 0, I1 * FB, bh);
-                        tma_reduce_add_3d(&tmAcc, slot + F_DSP / 2 + 8192, 32, I1 * FB, bh);
+                fin_store();  // the block loaded at the previous pair
+                if (leader) {
+                    if (SPION_FDBG_NODQ) {
+                        mbar_arrive(ds_empty + acc);
+                    } else {
+                        const int I0 = rows[pj], I1 = paired ? rows[pj + 1] : 0;
+                        tma_reduce_add_3d(&tmAcc, slot, 0, I0 * FB, bh);
+                        tma_reduce_add_3d(&tmAcc, slot + 8192, 32, I0 * FB, bh);
+                        if (paired) {
+                            tma_reduce_add_3d(&tmAcc, slot + F_DSP / 2, 0, I1 * FB, bh);
+                            tma_reduce_add_3d(&tmAcc, slot + F_DSP / 2 + 8192, 32, I1 * FB, bh);
+                        }
+                        bulk_commit();
+                        bulk_wait_read<0>();  // staged rows consumed: the softmax may refill the buffer
+                        mbar_arrive(ds_empty + acc);
+                        bulk_wait<1>();       // the previous pair's reductions are complete
+                        if (!SPION_FDBG_NOFIN) complete_a();
+                        a_n = paired ? 2 : 1; a_bh = bh; a_I0 = I0; a_I1 = I1;
                     }
-                    bulk_commit();
-                    bulk_wait_read<0>();          // staged rows consumed: the softmax may refill the buffer
-                    mbar_arrive(ds_empty + acc);
-                    bulk_wait<1>();               // the previous pair's reductions are complete
-                    count_completed(prev_n, prev_bh, prev_I0, prev_I1);
-                    prev_n = paired ? 2 : 1;
-                    prev_bh = bh;
-                    prev_I0 = I0;
-                    prev_I1 = I1;
                 }
                 named_bar_sync(BAR_DQ, 128);
-                finalize();
+                if (!SPION_FDBG_NOFIN) {
+                    const int tail = fq[1];
+                    while (tail - f_head > FQ / 2) {     // backlog (bursts of completions): catch up now
+                        fin_load(tail);
+                        fin_store();
+                    }
+                    fin_load(tail);
+                }
                 ++gp;
             }
             sched_release(sc, ks, true);
         }
-        if (leader) {
+        // drain: the last pair's reductions, every pending count, every queued block
+        if (leader && !SPION_FDBG_NODQ && !SPION_FDBG_NOFIN) {
             bulk_wait<0>();
-            count_completed(prev_n, prev_bh, prev_I0, prev_I1);
+            complete_a();
+            flush();      // the last batch of atomics ...
+            consume_r();  // ... and its results
         }
         named_bar_sync(BAR_DQ, 128);
-        finalize();
+        if (!SPION_FDBG_NOFIN) {
+            const int tail = fq[1];
+            fin_store();
+            while (f_head < tail) {
+                fin_load(tail);
+                fin_store();
+            }
+        }
     } else {
         // ------------------------------------------------------------ softmax / dK-dV epilogue
-        regs_inc<176>();
+        regs_inc<168>();
         const int r = (warp & 3) * 32 + lane;  // key row of the tile = TMEM lane
         const int wg = warp >> 2;              // warpgroup: even (0) / odd (1) entries of an item
         const int slot = r / FB;

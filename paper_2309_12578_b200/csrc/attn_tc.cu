@@ -57,6 +57,9 @@ __host__ __device__ constexpr int bwd_threads(int mw, int nsw) { return 32 * (mw
 #ifndef SPION_FWD_NST32
 #define SPION_FWD_NST32 8
 #endif
+#ifndef SPION_DKV_ACCB  // dK/dV accumulator pairs where one CTA owns the SM (1: epilogue not deferred)
+#define SPION_DKV_ACCB 1
+#endif
 template <int B> struct Cfg {
     static constexpr int FWD_CTAS = 2, FWD_COLS = 256;
     static constexpr int FWD_NBUF = (256 - 64) / B;      // S/P buffers of B columns + O
@@ -65,7 +68,11 @@ template <int B> struct Cfg {
     static constexpr int DQ_NBUF = (DQ_COLS - 64) / (2 * B);   // S+dP buffers + dQ
     static constexpr int DQ_NST = B == 32 ? 3 : 8;             // K_J + V_J per stage
     static constexpr int DKV_CTAS = B == 32 ? SPION_DKV_CTAS32 : 1, DKV_COLS = 512 / DKV_CTAS;
-    static constexpr int DKV_NBUF = (DKV_COLS - 128) / (2 * B);  // S^T+dP^T buffers + dK, dV
+    // dK/dV accumulator pairs: two where one CTA owns the SM, so an item's epilogue (deferred by the
+    // softmax warps until after their first block of the next item) never waits on, nor stalls, the
+    // tensor pipe; S^T+dP^T buffers take the rest of the columns
+    static constexpr int DKV_ACCB = DKV_CTAS == 1 ? SPION_DKV_ACCB : 1;
+    static constexpr int DKV_NBUF = (DKV_COLS - 128 * DKV_ACCB) / (2 * B);
     static constexpr int DKV_NST = B == 32 ? SPION_DKV_NST32 : 7;  // Q_I + dO_I + lse_I + D_I per stage
     // K/V (and dK/dV staging) buffers across items: three where one CTA owns the SM, so the next
     // item's K/V can load while the previous item's dK/dV store still holds its buffer
@@ -440,6 +447,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
     constexpr uint32_t BUFW = 2 * B;  // S at b*BUFW, dP at b*BUFW + B
     constexpr uint32_t COL_DQ = NBUF * BUFW;
+    // Q and dO of the item copied into TMEM (tcgen05.cp) where the columns allow: S = Q K_J^T and
+    // dP = dO V_J^T then run as TS MMAs (A from tensor memory), reading only K_J / V_J from shared
+    // memory (SS MMAs at N = 64 are shared-memory bound: 48 vs 32 cycles per K = 16 step)
+    constexpr bool TSQ = SPION_DQ_TS && (NBUF * BUFW + 64 + 64 <= Cfg<B>::DQ_COLS);
+    constexpr uint32_t COL_QA = COL_DQ + 64, COL_DOA = COL_QA + 32;
     constexpr uint32_t KV_BYTES = B * 128, STG = 2 * KV_BYTES;
     constexpr uint32_t IDESC_S = idesc_bf16(128, B, false, false);   // S = Q K^T, dP = dO V^T
     constexpr uint32_t IDESC_DQ = idesc_bf16(128, 64, false, true);  // dQ += dS K
@@ -577,6 +589,14 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
                 const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
+                if (TSQ && elect_one()) {  // in issue order with the MMAs below (and the last item's)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        tmem_cp_128x256b(tmem + COL_QA + 8 * k, dQ0 + 2 * k);
+                        tmem_cp_128x256b(tmem + COL_DOA + 8 * k, ddO0 + 2 * k);
+                    }
+                }
+                __syncwarp();
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
                     if (NSW > 1 && (int)b != sw) {
@@ -592,10 +612,18 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
                     const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + sst * STG + KV_BYTES));
                     if (elect_one()) {
+                        if (TSQ) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                            for (int k = 0; k < 4; ++k) MMA_TS(tmem + cs, tmem + COL_QA + 8 * k, dK0 + 2 * k, IDESC_S, k > 0);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
+                            for (int k = 0; k < 4; ++k)
+                                MMA_TS(tmem + cs + B, tmem + COL_DOA + 8 * k, dV0 + 2 * k, IDESC_S, k > 0);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs + B, ddO0 + 2 * k, dV0 + 2 * k, IDESC_S, k > 0);
+                        }
                         mma_commit(s_full + 2 * b + (PP ? (sj & 1) : 0));
                     }
                     __syncwarp();
@@ -796,12 +824,12 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcParams p) {
     constexpr int NST = Cfg<B>::DKV_NST, NBUF = Cfg<B>::DKV_NBUF, MW = Cfg<B>::DKV_MW, NSW = Cfg<B>::DKV_NSW;
-    constexpr int KVB = Cfg<B>::DKV_KVB;
+    constexpr int KVB = Cfg<B>::DKV_KVB, ACCB = Cfg<B>::DKV_ACCB;
     constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
     constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
     constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
     constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
-    constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;
+    constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;  // + 128 * accumulator pair
     constexpr uint32_t TILE = B * 128;
     constexpr uint32_t STAGE = 2 * TILE + 1024;  // Q_I, dO_I, lse_I, D_I
     constexpr uint32_t IDESC_ST = idesc_bf16(128, B, false, false);   // S^T = K Q^T, dP^T = V dO^T
@@ -813,12 +841,12 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     uint8_t *sStage = smem + KVB * 32768;
     uint8_t *sSched = sStage + NST * STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sSched + SCHED_BYTES);
-    uint64_t *kv_full = bars + 0, *kv_empty = bars + 3, *acc_full = bars + 6, *s_full = bars + 7,
+    uint64_t *kv_full = bars + 0, *kv_empty = bars + 3, *acc_full = bars + 6, *s_full = bars + 8,
              *p_full = s_full + 2 * NBUF, *freeb = p_full + NBUF, *q_full = freeb + NBUF, *q_empty = q_full + NST;
     Sched sc = make_sched(sSched, q_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
     uint64_t *staged = q_empty + NST + 9;  // [KVB]: dK/dV of the item using K/V buffer kb staged there
-    uint64_t *acc_empty = staged + 3;      // the epilogue has read the dK/dV accumulators
+    uint64_t *acc_empty = staged + 3;      // [ACCB]: the epilogue has read accumulator pair a
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -829,10 +857,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         // per (buffer, consumer), so each has one in-order producer and one in-order consumer
         for (int i = 0; i < 2 * NBUF; ++i) mbar_init(s_full + i, 1);
         for (int i = 0; i < NBUF; ++i) { mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
-        mbar_init(acc_full, 1);
+        for (int i = 0; i < ACCB; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, 32 * MW); }
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
         for (int i = 0; i < KVB; ++i) mbar_init(staged + i, 32 * MW);
-        mbar_init(acc_empty, 32 * MW);
         sched_init(sc, 2 + NSW + MW);
         fence_barrier_init();
     }
@@ -993,8 +1020,10 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             if (h[0] < 0) break;
             const int cnt = h[3];
             if (cnt > 0) {
-                if (na > 0) mbar_wait(acc_empty, (na - 1) & 1);  // the last item's dK/dV were read
+                const int ab = na % ACCB;  // accumulator pair of this item
+                if (na >= ACCB) mbar_wait(acc_empty + ab, ((na / ACCB) - 1) & 1);  // its last user was read
                 ++na;
+                const uint32_t cdk = COL_DK + 128 * ab, cdv = COL_DV + 128 * ab;
                 for (int pj = 0; pj < cnt; ++pj) {
                     const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
                     if (lane == 0) tr.ev(30);
@@ -1009,16 +1038,16 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         tr.ev(31);
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            MMA_TS(tmem + COL_DV, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
+                            MMA_TS(tmem + cdv, tmem + cs + 32 * (k / 2) + 8 * (k % 2), ddO0 + 128 * k, IDESC_DKV,
                                         (pj > 0) || (k > 0));
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
-                            MMA_TS(tmem + COL_DK, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
+                            MMA_TS(tmem + cdk, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
                                         (pj > 0) || (k > 0));
                         tr.ev(32);
                         mma_commit(freeb + b);
                         mma_commit(q_empty + pst);
-                        if (pj == cnt - 1) mma_commit(acc_full);
+                        if (pj == cnt - 1) mma_commit(acc_full + ab);
                         tr.ev(33);
                     }
                     __syncwarp();
@@ -1063,11 +1092,53 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         const int wg = warp >> 2;              // warpgroup: alternate blocks (MW = 8); epilogue halves
         const int slot = r / B;
         const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        uint32_t a_ph = 0, ph = 0, g = 0, sph = 0;  // sph: phase bit per score buffer (this warpgroup's uses)
-        int st = 0, nk = 0;
+        uint32_t ph = 0, g = 0, sph = 0;  // sph: phase bit per score buffer (this warpgroup's uses)
+        int st = 0, nk = 0, na = 0;
         const float sl2 = p.scale_log2;
         Tracer tr(p, 2 + (threadIdx.x == 128));
         const bool trc = threadIdx.x == 0 || threadIdx.x == 128;
+        // pending epilogue: K/V buffer (staging) and accumulator pair of an item whose blocks are done
+        int dfr_kb = -1, dfr_ab = 0;
+        uint32_t dfr_par = 0;
+        auto epilogue = [&]() {
+            if (dfr_kb < 0) return;
+            mbar_wait(acc_full + dfr_ab, dfr_par);
+            if (trc) tr.ev(23);
+            tc_fence_after();
+            // dK, dV -> bf16 staged in the item's K/V buffer (free: every S^T/dP^T MMA is done),
+            // then one TMA store per tile (coalesced; rows past L clipped)
+            uint8_t *sdK = sKV + dfr_kb * 32768, *sdV = sdK + 16384;
+            const uint32_t cdk = COL_DK + 128 * dfr_ab, cdv = COL_DV + 128 * dfr_ab;
+            if (MW == 8) {  // warpgroup 0 stages dK, warpgroup 1 stages dV
+                const uint32_t col = wg == 0 ? cdk : cdv;
+                uint8_t *dst = wg == 0 ? sdK : sdV;
+                const float f = wg == 0 ? p.scale : 1.f;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    float w[32];
+                    tmem_ld32(tl + col + hh * 32, w);
+                    tmem_ld_wait();
+                    stage_row_bf16(dst, r, w, f, hh);
+                }
+            } else {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    float kv[32], vv[32];
+                    tmem_ld32(tl + cdk + hh * 32, kv);
+                    tmem_ld32(tl + cdv + hh * 32, vv);
+                    tmem_ld_wait();
+                    stage_row_bf16(sdK, r, kv, p.scale, hh);
+                    stage_row_bf16(sdV, r, vv, 1.f, hh);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(acc_empty + dfr_ab);  // a later item's first dV/dK MMAs may overwrite the pair
+            fence_proxy_async_smem();         // generic-proxy writes -> the TMA store (async proxy)
+            mbar_arrive(staged + dfr_kb);
+            tc_fence_before();
+            if (trc) tr.ev(24);
+            dfr_kb = -1;
+        };
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -1147,47 +1218,22 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 mbar_arrive(p_full + sb);
                 if (trc) tr.ev(22);
                 if (++st == NST) { st = 0; ph ^= 1; }
+                epilogue();  // the previous item's (deferred), after this item's first block
             }
-            mbar_wait(acc_full, a_ph);
-            if (trc) tr.ev(23);
-            a_ph ^= 1;
-            tc_fence_after();
-            // dK, dV -> bf16 staged in this item's K/V buffer (free: every S^T/dP^T MMA is done),
-            // then one TMA store per tile (coalesced; rows past L clipped)
-            const int kb = nk % KVB;
+            epilogue();  // (no block of this warpgroup in this item)
+            // this item's epilogue: now (one accumulator pair), or deferred until after this warpgroup's
+            // first block of the next item (two pairs: the tensor pipe is busy with the next item's
+            // score MMAs, so waiting here for the last dV/dK MMAs would idle the softmax warps)
+            dfr_kb = nk % KVB;
+            dfr_ab = na % ACCB;
+            dfr_par = (uint32_t)(na / ACCB) & 1;
             ++nk;
-            uint8_t *sdK = sKV + kb * 32768, *sdV = sdK + 16384;
-            if (MW == 8) {  // warpgroup 0 stages dK, warpgroup 1 stages dV
-                const uint32_t col = wg == 0 ? COL_DK : COL_DV;
-                uint8_t *dst = wg == 0 ? sdK : sdV;
-                const float f = wg == 0 ? p.scale : 1.f;
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    float w[32];
-                    tmem_ld32(tl + col + hh * 32, w);
-                    tmem_ld_wait();
-                    stage_row_bf16(dst, r, w, f, hh);
-                }
-            } else {
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    float kv[32], vv[32];
-                    tmem_ld32(tl + COL_DK + hh * 32, kv);
-                    tmem_ld32(tl + COL_DV + hh * 32, vv);
-                    tmem_ld_wait();
-                    stage_row_bf16(sdK, r, kv, p.scale, hh);
-                    stage_row_bf16(sdV, r, vv, 1.f, hh);
-                }
-            }
-            tc_fence_before();
-            mbar_arrive(acc_empty);    // the next item's first dV/dK MMAs may overwrite the accumulators
-            fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
-            mbar_arrive(staged + kb);
-            tc_fence_before();
-            if (trc) tr.ev(24);
+            ++na;
+            if (ACCB == 1) epilogue();
             g += cnt;
             sched_release(sc, ks, true);
         }
+        epilogue();  // the last item's
     }
     __syncthreads();
     sched_finish(p, t_start);

@@ -30,6 +30,9 @@
 #ifndef SPION_NSW  // 1: one S-MMA warp per buffer where one CTA owns the SM (0: a single S-MMA warp)
 #define SPION_NSW 0
 #endif
+#ifndef SPION_DQ_TS  // dQ pass: Q / dO of the item in tensor memory (TS score MMAs) where TMEM allows
+#define SPION_DQ_TS 1
+#endif
 #ifndef SPION_DBG_NOLOAD  // per-block operand tiles not loaded
 #define SPION_DBG_NOLOAD 0
 #endif

@@ -186,6 +186,12 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// shared -> tensor memory copy of 128 rows x 256 bits (one K = 16 chunk of a SW128 K-major bf16
+// operand tile, described like an MMA operand): lands in the A-operand layout of a TS MMA (row i =
+// lane i, two bf16 per column).  Asynchronous, in issue order with this thread's tcgen05.mma.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 // arrive on an mbarrier once every previously issued tcgen05 op of this thread completes
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
