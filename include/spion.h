@@ -291,9 +291,29 @@ SPION_API spion_status spion_score_mean(const void *Q_dev, const void *K_dev, in
 SPION_API spion_status spion_transition(const double *sumsq_dev, double alpha, int32_t *switch_dev,
                                         double *dist_dev, int32_t *switch_host, void *stream);
 
+/* the projections of the sparse-MHA sub-layer (Alg. 5 l.2-3,
+ * l.8-9) on the tensor cores, with the head split / concatenation
+ * folded into the operand and output addressing:
+ *   C[M][N] = alpha * A[M][K] B[N][K]^T, bf16 in, fp32 accumulation, bf16 out.
+ * B: [N][K] row-major (a weight in nn.Linear layout, out x in).  A and C are
+ * either SPION_GEMM_ROWMAJOR ([M][K], [M][N] contiguous) or SPION_GEMM_HEADS:
+ * the attention layout, W tensors [batch*H][L][64] bf16 stacked contiguously
+ * (tensor w at element offset w*batch*H*L*64), row m = token (b, l) with
+ * M = batch*L, column (A: k, C: n) = w*H*64 + h*64 + e.  So Q|K|V = X W^T with
+ * c_layout = HEADS writes the three attention inputs directly (W = 3), and
+ * S Wo^T with a_layout = HEADS reads the attention output directly (W = 1).
+ * Needs M % 128 == 0, N % 128 == 0, K % 64 == 0 (else UNSUPPORTED); with a
+ * HEADS layout also head dim 64, L % 128 == 0 and M == batch*L, K (or N) a
+ * multiple of 64*H (else SHAPE).  16-byte aligned pointers.  L, H, batch are
+ * ignored for two ROWMAJOR operands.  Persistent tcgen05 kernel: 128 x 128
+ * tiles, TMA operand ring, TMEM accumulators, TMA stores. */
+typedef enum { SPION_GEMM_ROWMAJOR = 0, SPION_GEMM_HEADS = 1 } spion_gemm_layout;
+SPION_API spion_status spion_gemm_bf16(const void *A_dev, const void *B_dev, void *C_dev, int32_t M, int32_t N,
+                                       int32_t K, int32_t a_layout, int32_t c_layout, int32_t L, int32_t H,
+                                       int32_t batch, float alpha, void *stream);
+
 /* the sparse-MHA sub-layer around the attention (Alg. 5,
- * P:655-674).  The projections Q,K,V = X W^{Q,K,V} (l.2) and S W^O (l.9) are plain
- * GEMMs done by the caller (cuBLAS).
+ * P:655-674): head split / concatenation and dropout + residual kernels.
  * spion_mha_heads: l.3 split / l.8 concatenate.  packed_dev: [batch][L][W][H][d]
  * bf16 row-major (the projection output, W tensors side by side: W = 3 for
  * Q|K|V, 1 for the concatenated heads); heads_dev: W tensors [batch*H][L][d],

@@ -13,6 +13,7 @@ STATUS = {0: "ok", 1: "shape", 2: "param", 3: "data", 4: "align", 5: "workspace"
 F32, BF16 = 0, 1
 PATH_CUDA_CORE, PATH_TCGEN05 = 0, 1  # spion_attn_path
 BWD_DETERMINISTIC, BWD_FUSED = 1, 2  # spion_attn_bwd_ex flags
+GEMM_ROWMAJOR, GEMM_HEADS = 0, 1  # spion_gemm_bf16 layouts
 SOFTMAX = {"paper": 0, "masked": 1}
 THRESH = {"linear": 0, "nearest": 1, "absolute": 2}
 # spion_pattern_flags (include/spion.h): SPION-C, prose recursion, all-cells seeding
@@ -46,6 +47,9 @@ EXPORTS = {
     "spion_pattern_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "spion_mha_heads": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
+    "spion_gemm_bf16": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_float, ctypes.c_void_p]),
     "spion_dropout_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                               ctypes.c_float, ctypes.c_uint64, ctypes.c_void_p]),
     "spion_score_mean_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]),

@@ -633,6 +633,29 @@ spion_status spion_transition(const double *sumsq_dev, double alpha, int32_t *sw
 }
 
 // ------------------------------------------------------------------ NEXT-4: sparse-MHA sub-layer
+spion_status spion_gemm_bf16(const void *A_dev, const void *B_dev, void *C_dev, int32_t M, int32_t N, int32_t K,
+                             int32_t a_layout, int32_t c_layout, int32_t L, int32_t H, int32_t batch, float alpha,
+                             void *stream) {
+    if (!A_dev || !B_dev || !C_dev) return SPION_ERR_PARAM;
+    if (M <= 0 || N <= 0 || K <= 0) return SPION_ERR_SHAPE;
+    if ((a_layout != SPION_GEMM_ROWMAJOR && a_layout != SPION_GEMM_HEADS) ||
+        (c_layout != SPION_GEMM_ROWMAJOR && c_layout != SPION_GEMM_HEADS))
+        return SPION_ERR_PARAM;
+    if (!aligned16(A_dev) || !aligned16(B_dev) || !aligned16(C_dev)) return SPION_ERR_ALIGN;
+    if (M % 128 || N % 128 || K % 64) return SPION_ERR_UNSUPPORTED;
+    const bool heads = a_layout == SPION_GEMM_HEADS || c_layout == SPION_GEMM_HEADS;
+    if (heads) {
+        if (L <= 0 || H <= 0 || batch <= 0) return SPION_ERR_SHAPE;
+        if (L % 128 || (int64_t)batch * L != M) return SPION_ERR_SHAPE;
+        if (a_layout == SPION_GEMM_HEADS && K % (64 * H)) return SPION_ERR_SHAPE;
+        if (c_layout == SPION_GEMM_HEADS && N % (64 * H)) return SPION_ERR_SHAPE;
+        if ((int64_t)batch * H > 65535 * 4) return SPION_ERR_UNSUPPORTED;
+    }
+    if (!tc_encode_fn_available()) return SPION_ERR_UNSUPPORTED;
+    return launch_gemm_bf16(A_dev, B_dev, C_dev, M, N, K, a_layout == SPION_GEMM_HEADS, c_layout == SPION_GEMM_HEADS,
+                            L, H, batch, alpha, static_cast<cudaStream_t>(stream));
+}
+
 spion_status spion_mha_heads(void *packed_dev, void *heads_dev, int64_t batch, int32_t L, int32_t W, int32_t H,
                              int32_t d, int32_t to_heads, void *stream) {
     if (!packed_dev || !heads_dev) return SPION_ERR_PARAM;

@@ -29,6 +29,7 @@ spion_status launch_bwd_simt(const AttnArgs &a, spion_dtype dt, cudaStream_t s);
 
 // tensor-core (tcgen05) path; attn_tc.cu
 bool tc_supported(const AttnArgs &a, spion_dtype dt);
+bool tc_encode_fn_available();  // the driver's cuTensorMapEncodeTiled was found
 spion_status launch_fwd_tc(const AttnArgs &a, cudaStream_t s);
 spion_status launch_bwd_tc(const AttnArgs &a, cudaStream_t s);
 
@@ -48,6 +49,10 @@ spion_status launch_score_mean(const void *Q, const void *K, const float *lse, i
 int score_splits(int64_t bh, int L);
 // Alg. 2 / Eq. 2 transition test on three device sums of squares; scores.cu
 spion_status launch_transition(const double *sumsq, double alpha, int32_t *flag, double *dist, cudaStream_t s);
+
+// NEXT-4 projection GEMM (tcgen05; head-layout operand gather / output scatter); gemm.cu
+spion_status launch_gemm_bf16(const void *A, const void *B, void *C, int M, int N, int K, int a_heads, int c_heads,
+                              int L, int H, int batch, float alpha, cudaStream_t s);
 
 // NEXT-4 sub-layer kernels; mha.cu
 spion_status launch_heads_permute(const void *src, void *dst, int64_t batch, int L, int W, int H, int d, int to_heads,

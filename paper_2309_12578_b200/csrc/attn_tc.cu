@@ -1306,6 +1306,8 @@ bool tc_make_map(void *map, const void *base, int L, int64_t bh, int64_t stride_
     return tc_map(static_cast<CUtensorMap *>(map), base, L, bh, stride_bh, stride_l, box_rows);
 }
 
+bool tc_encode_fn_available() { return tc_encode_fn() != nullptr; }
+
 bool tc_supported(const AttnArgs &a, spion_dtype dt) {
     if (dt != SPION_BF16 || a.d != 64 || !(a.B == 32 || a.B == 64) || !a.plan) return false;
     if (a.stride_l % 8 || a.stride_bh % 8) return false;

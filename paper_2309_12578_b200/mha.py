@@ -3,10 +3,15 @@
     S = concat_h( SparseAttention(Q_h, K_h, V_h, P) ),  Q|K|V = X W^{QKV}      (Alg. 5 l.2-8)
     O = dropout(S W^O) + E                                                      (Alg. 5 l.9)
 
-The head split / concatenation and the dropout + residual run in this library's kernels
-(`spion_mha_heads`, `spion_dropout_residual`), the attention in the tcgen05 kernels; the two
-projections are plain GEMMs (torch.matmul -> cuBLAS).  Alg. 5 l.1 (LayerNorm) belongs to the
-encoder around it and is not part of this sub-layer.  bf16 throughout; autograd-complete.
+The projections run on this library's tcgen05 GEMM (`spion_gemm_bf16`) with the head split /
+concatenation folded into its addressing: Q|K|V = X W^{QKV}^T stores the attention inputs
+[3][batch*H][L][64] straight from the GEMM epilogue (l.2-3), and S W^O^T reads the attention output
+[batch*H][L][64] straight into the GEMM (l.8-9); their backward activation GEMMs (dS = dY W^O and
+dX = dQKV W^{QKV}) use the same layouts.  The weight gradients are cuBLAS GEMMs over the
+concatenated activations (one head-merge pass each).  The dropout + residual of l.9 is one kernel
+(`spion_dropout_residual`), the attention the tcgen05 SPION kernels.  Weights in nn.Linear layout
+(out x in).  Alg. 5 l.1 (LayerNorm) belongs to the encoder around it and is not part of this
+sub-layer.  bf16 throughout; autograd-complete.
 """
 from __future__ import annotations
 
@@ -93,6 +98,96 @@ class _DropoutResidual(torch.autograd.Function):
         return dy, g, None, None
 
 
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, m: int, n: int, k: int, a_heads: bool = False,
+         c_heads: bool = False, L: int = 0, H: int = 0, batch: int = 0, alpha: float = 1.0) -> torch.Tensor:
+    """out = alpha * A B^T on the tcgen05 GEMM (spion_gemm_bf16); A / out row-major or in the attention
+    layout [W][batch*H][L][64] (a_heads / c_heads); b: [N][K] row-major."""
+    spion._require_cuda(a, b, out)
+    for t in (a, b, out):
+        if t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError("gemm: contiguous bf16 tensors")
+    lay = lambda heads: N.GEMM_HEADS if heads else N.GEMM_ROWMAJOR
+    st = N.lib().spion_gemm_bf16(spion._p(a), spion._p(b), spion._p(out), m, n, k, lay(a_heads), lay(c_heads), L, H,
+                                 batch, float(alpha), spion._stream(a.device))
+    N.check(st, "spion_gemm_bf16")
+    return out
+
+
+def _stacked(dq, dk, dv):
+    """(dQ, dK, dV) as one [3][bh][L][d] tensor: a zero-copy view when they are consecutive slices of
+    one buffer (the attention backward allocates them that way), else a copy."""
+    sz = dq.numel() * dq.element_size()
+    if (dq.is_contiguous() and dk.is_contiguous() and dv.is_contiguous() and dq.shape == dk.shape == dv.shape
+            and dk.data_ptr() == dq.data_ptr() + sz and dv.data_ptr() == dk.data_ptr() + sz):
+        return dq.as_strided((3,) + tuple(dq.shape), (dq.numel(),) + tuple(dq.stride()))
+    return torch.stack([dq, dk, dv]).contiguous()
+
+
+class _QKVProjection(torch.autograd.Function):
+    """Alg. 5 l.2-3: E [batch][L][D] -> Q, K, V [batch*H][L][d] = heads of E W_qkv^T (W_qkv [3D][D])."""
+
+    @staticmethod
+    def forward(ctx, e, w_qkv, H: int):
+        batch, L, D = e.shape
+        d = D // H
+        ec = e.contiguous()
+        qkv = torch.empty((3, batch * H, L, d), dtype=e.dtype, device=e.device)
+        gemm(ec, w_qkv.contiguous(), qkv, batch * L, 3 * D, D, c_heads=True, L=L, H=H, batch=batch)
+        ctx.save_for_backward(ec, w_qkv)
+        ctx.dims = (batch, L, D, H)
+        return qkv[0], qkv[1], qkv[2]
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        e, w_qkv = ctx.saved_tensors
+        batch, L, D, H = ctx.dims
+        d = D // H
+        z = lambda x: x if x is not None else torch.zeros((batch * H, L, d), dtype=e.dtype, device=e.device)
+        g = _stacked(z(dq), z(dk), z(dv))
+        de = torch.empty((batch, L, D), dtype=e.dtype, device=e.device)
+        gemm(g, w_qkv.t().contiguous(), de, batch * L, D, 3 * D, a_heads=True, L=L, H=H, batch=batch)
+        packed = torch.empty((batch, L, 3 * D), dtype=e.dtype, device=e.device)
+        _heads(packed, g, batch, L, 3, H, d, False)
+        dw = packed.view(batch * L, 3 * D).t() @ e.view(batch * L, D)  # weight gradient (cuBLAS)
+        return de, dw, None
+
+
+class _OutProjection(torch.autograd.Function):
+    """Alg. 5 l.8-9: heads S [batch*H][L][d] -> concat_h(S) W_o^T [batch][L][D] (W_o [D][D])."""
+
+    @staticmethod
+    def forward(ctx, s, w_o, batch: int, H: int):
+        bh, L, d = s.shape
+        D = H * d
+        sc = s.contiguous()
+        y = torch.empty((batch, L, D), dtype=s.dtype, device=s.device)
+        gemm(sc, w_o.contiguous(), y, batch * L, D, D, a_heads=True, L=L, H=H, batch=batch)
+        ctx.save_for_backward(sc, w_o)
+        ctx.dims = (batch, L, D, H)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        s, w_o = ctx.saved_tensors
+        batch, L, D, H = ctx.dims
+        d = D // H
+        dyc = dy.contiguous()
+        ds = torch.empty((batch * H, L, d), dtype=s.dtype, device=s.device)
+        gemm(dyc, w_o.t().contiguous(), ds, batch * L, D, D, c_heads=True, L=L, H=H, batch=batch)
+        packed = torch.empty((batch, L, D), dtype=s.dtype, device=s.device)
+        _heads(packed, s, batch, L, 1, H, d, False)
+        dw = dyc.view(batch * L, D).t() @ packed.view(batch * L, D)  # weight gradient (cuBLAS)
+        return ds, dw, None, None
+
+
+def qkv_projection(e: torch.Tensor, w_qkv: torch.Tensor, H: int):
+    return _QKVProjection.apply(e, w_qkv, H)
+
+
+def out_projection(s: torch.Tensor, w_o: torch.Tensor, batch: int, H: int):
+    return _OutProjection.apply(s, w_o, batch, H)
+
+
 def split_heads(qkv: torch.Tensor, H: int):
     return _SplitHeads.apply(qkv, H)
 
@@ -119,16 +214,16 @@ class SparseMHA(torch.nn.Module):
         self.D, self.H, self.d, self.p, self.mode = D, H, D // H, dropout, mode
         g = torch.Generator(device="cpu").manual_seed(seed)
         s = 1.0 / math.sqrt(D)
-        self.w_qkv = torch.nn.Parameter((torch.randn(D, 3 * D, generator=g) * s).to(device=device, dtype=dtype))
+        # nn.Linear layout (out x in): Q|K|V = E W_qkv^T, Y = S W_o^T
+        self.w_qkv = torch.nn.Parameter((torch.randn(3 * D, D, generator=g) * s).to(device=device, dtype=dtype))
         self.w_o = torch.nn.Parameter((torch.randn(D, D, generator=g) * s).to(device=device, dtype=dtype))
         self.step = 0
 
     def forward(self, e: torch.Tensor, bp: spion.BlockPattern, seed: Optional[int] = None) -> torch.Tensor:
         batch, L, D = e.shape
-        qkv = e @ self.w_qkv                                          # l.2 (cuBLAS)
-        q, k, v = split_heads(qkv, self.H)                            # l.3
+        q, k, v = qkv_projection(e, self.w_qkv, self.H)               # l.2-3 (tcgen05 GEMM -> heads)
         s = spion.attention(q, k, v, bp, self.mode)                   # l.4-7 (tcgen05 kernels)
-        y = merge_heads(s, batch, self.H) @ self.w_o                  # l.8-9 (cuBLAS)
+        y = out_projection(s, self.w_o, batch, self.H)                # l.8-9 (heads -> tcgen05 GEMM)
         if seed is None:
             seed, self.step = self.step, self.step + 1
         p = self.p if self.training else 0.0

@@ -251,7 +251,11 @@ class _SparseAttention(torch.autograd.Function):
         q, k, v, o, lse = ctx.saved_tensors
         if do.stride() != q.stride():  # the kernels take one layout for every tensor: materialise q's
             do = torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device).copy_(do)
-        dq, dk, dv = attn_bwd(q, k, v, o, do, lse, ctx.bp, ctx.mode, ctx.scale)
+        if q.is_contiguous():  # dQ, dK, dV as slices of one buffer (a zero-copy [3][bh][L][d] for the QKV GEMM)
+            g = torch.empty((3,) + tuple(q.shape), dtype=q.dtype, device=q.device)
+            dq, dk, dv = attn_bwd(q, k, v, o, do, lse, ctx.bp, ctx.mode, ctx.scale, dq=g[0], dk=g[1], dv=g[2])
+        else:
+            dq, dk, dv = attn_bwd(q, k, v, o, do, lse, ctx.bp, ctx.mode, ctx.scale)
         return dq, dk, dv, None, None, None
 
 

@@ -62,7 +62,7 @@ def _reference(e, w_qkv, w_o, fl, B, H, mode):
     """Alg. 5 with torch ops in fp32: dense masked attention from the block mask."""
     batch, L, D = e.shape
     d = D // H
-    qkv = e @ w_qkv
+    qkv = e @ w_qkv.t()  # nn.Linear layout (out x in)
     q, k, v = qkv.view(batch, L, 3, H, d).permute(2, 0, 3, 1, 4)
     allowed = torch.from_numpy(np.kron(fl, np.ones((B, B)))).bool().to(e.device)
     s = (q @ k.transpose(-1, -2)) / math.sqrt(d)
@@ -74,7 +74,35 @@ def _reference(e, w_qkv, w_o, fl, B, H, mode):
     else:
         p = torch.softmax(s, -1)
     o = (p @ v).permute(0, 2, 1, 3).reshape(batch, L, D)
-    return o @ w_o + e
+    return o @ w_o.t() + e
+
+
+@pytest.mark.parametrize("M,N,K,a_heads,c_heads,batch,L,H", [
+    (256, 256, 128, False, False, 1, 256, 2),      # plain row-major
+    (1024, 384, 192, False, False, 1, 1024, 1),    # several N tiles, K = 3 steps
+    (2 * 512, 3 * 256, 256, False, True, 2, 512, 4),  # QKV: scatter into [3][batch*H][L][64]
+    (2 * 512, 256, 256, True, False, 2, 512, 4),      # out-projection: gather from [batch*H][L][64]
+    (3 * 256, 256, 3 * 128, True, False, 3, 256, 2),  # dX: gather from [3][batch*H][L][64]
+    (4 * 128, 128, 128, False, True, 4, 128, 2),      # dS: scatter, L = 128 (one tile per batch item)
+])
+def test_gemm_bf16_layouts(M, N, K, a_heads, c_heads, batch, L, H):
+    """spion_gemm_bf16 (tcgen05) against torch fp32 matmul, with the head-layout gather / scatter
+    checked against explicit permutes."""
+    mha, spion = _mods()
+    torch.manual_seed(M + N + K)
+    a2 = torch.randn(M, K, device=DEV).bfloat16()
+    b = (torch.randn(N, K, device=DEV) / math.sqrt(K)).bfloat16()
+    ref = a2.float() @ b.float().t()
+    to_heads = lambda x, W: x.view(batch, L, W, H, 64).permute(2, 0, 3, 1, 4).contiguous()  # [W][batch][H][L][64]
+    a = to_heads(a2, K // (64 * H)) if a_heads else a2
+    out = torch.empty((N // (64 * H), batch * H, L, 64) if c_heads else (M, N), device=DEV, dtype=torch.bfloat16)
+    c0 = spion.tc_launch_count()
+    mha.gemm(a, b, out, M, N, K, a_heads=a_heads, c_heads=c_heads, L=L, H=H, batch=batch, alpha=1.0)
+    torch.cuda.synchronize()
+    assert spion.tc_launch_count() - c0 == 1
+    got = out.view(N // (64 * H), batch, H, L, 64).permute(1, 3, 0, 2, 4).reshape(M, N) if c_heads else out
+    err = (got.float() - ref).abs().max().item()
+    assert err <= 1e-2 * ref.abs().max().item() + 1e-2, err
 
 
 @pytest.mark.parametrize("mode", ["paper", "masked"])

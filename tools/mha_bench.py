@@ -27,14 +27,18 @@ for name, L, B, H, batch in [("image", 1024, 32, 4, 64), ("text", 4096, 64, 8, 1
         out = m(e, bp, seed=1)
         out.backward(g)
 
-    qkv = (e @ m.w_qkv).detach()
-    q, k, v = [x.contiguous() for x in mha.split_heads(qkv, H)]
+    q, k, v = [x.contiguous() for x in mha.qkv_projection(e.detach(), m.w_qkv.detach(), H)]
+    ed, wq = e.detach(), m.w_qkv.detach()
     parts = {
         "sub-layer fwd+bwd": t(step),
-        "QKV GEMM fwd (cuBLAS)": t(lambda: e @ m.w_qkv),
-        "split heads": t(lambda: mha.split_heads(qkv, H)),
+        "QKV projection (tcgen05 GEMM -> heads)": t(lambda: mha.qkv_projection(ed, wq, H)),
+        "QKV GEMM (cuBLAS, packed; reference)": t(lambda: ed @ wq.t()),
+        "out projection (heads -> tcgen05 GEMM)": t(lambda: mha.out_projection(q, m.w_o.detach(), batch, H)),
         "attention fwd": t(lambda: spion.attn_fwd(q, k, v, bp)),
         "merge heads": t(lambda: mha.merge_heads(q, batch, H)),
-        "dropout+residual": t(lambda: mha.dropout_residual(qkv[..., :D].contiguous(), e.detach(), 0.1, 1)),
+        "dropout+residual": t(lambda: mha.dropout_residual(q.view(batch, L, D), e.detach(), 0.1, 1)),
     }
+    M = batch * L
+    gf = 2 * M * 3 * D * D / parts["QKV projection (tcgen05 GEMM -> heads)"] / 1e9
+    print(name, "QKV projection TFLOP/s", round(gf, 1))
     print(name, f"L={L} D={D} batch={batch} nnzb={bp.nnzb}", {k: round(v, 4) for k, v in parts.items()})
