@@ -164,10 +164,15 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if torch.cuda.is_available():
+        backend = os.environ.get("SPION_BENCH_BACKEND", "nccl")  # "gloo": host-logic check of the N-rank path
+        if torch.cuda.is_available() and backend == "nccl":
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
+            # gloo (CPU tests, or every rank time-sharing the visible GPUs to exercise the N-rank path)
+            if torch.cuda.is_available():
+                local = local % torch.cuda.device_count()
+                torch.cuda.set_device(local)
             dist.init_process_group("gloo")
         return dist, rank, world, local
     return None, 0, 1, 0
