@@ -72,7 +72,10 @@ template <int B> struct Cfg {
     // softmax warps until after their first block of the next item) never waits on, nor stalls, the
     // tensor pipe; S^T+dP^T buffers take the rest of the columns
     static constexpr int DKV_ACCB = DKV_CTAS == 1 ? SPION_DKV_ACCB : 1;
-    static constexpr int DKV_NBUF = (DKV_COLS - 128 * DKV_ACCB) / (2 * B);
+    // K and V of the item copied into TMEM (tcgen05.cp) where one CTA owns the SM: S^T = K Q_I^T and
+    // dP^T = V dO_I^T then run as TS MMAs (A from tensor memory), at the cost of 64 columns
+    static constexpr bool DKV_TS = SPION_DKV_TS && DKV_CTAS == 1;
+    static constexpr int DKV_NBUF = (DKV_COLS - 128 * DKV_ACCB - (DKV_TS ? 64 : 0)) / (2 * B);
     static constexpr int DKV_NST = B == 32 ? SPION_DKV_NST32 : 7;  // Q_I + dO_I + lse_I + D_I per stage
     // K/V (and dK/dV staging) buffers across items: three where one CTA owns the SM, so the next
     // item's K/V can load while the previous item's dK/dV store still holds its buffer
@@ -144,6 +147,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 
     if (warp == W_PROD) {
         // ------------------------------------------------------------ scheduler + TMA producer
+        Tracer tr(p, 0);
         if (lane == 0) { prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV); prefetch_tmap(&tmO); }
         // The next item is fetched from the scheduler when the current one starts, and its Q tile
         // is issued as soon as a Q buffer frees up (tested between the current item's K/V stages),
@@ -181,10 +185,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const int *h = sc.hdr + (ks & 3) * 8;
             const int bh = h[1], cnt = h[3];
             const int *col = sc.col + (ks & 3) * SCHED_CAP;
+            if (lane == 0) tr.ev(1);
             for (int j = 0; j < cnt; ++j) {  // whole warp runs the loop; one elected lane issues the TMA
                 if (!ended && j == 2) { sched_fetch_end(sc, ks + 1, p, nf, true); ended = true; }
                 if (ended && !nissued) nissued = item_tile(ks + 1, false);
                 mbar_wait(kv_empty + st, ph ^ 1);
+                if (lane == 0) tr.ev(3);
                 if (elect_one()) {
                     if (SPION_DBG_NOLOAD) {
                         mbar_arrive(kv_full + st);
@@ -204,29 +210,36 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     } else if (warp == W_MMA) {
         // ------------------------------------------------------------ S issuer (converged warp,
         // one elected lane issues): S = Q K_J^T up to NBUF blocks ahead of the softmax
+        Tracer tr(p, 1);
         int sst = 0, nq = 0;
         uint32_t sph = 0, g = 0;  // global block counter (buffer = g % NBUF)
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
+            if (lane == 0) tr.ev(10);
             const int cnt = h[3];
             if (cnt > 0) {
                 const int qb = nq & 1;
                 mbar_wait(q_full + qb, (nq >> 1) & 1);
+                if (lane == 0) tr.ev(11);
                 tc_fence_after();
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
                     mbar_wait(kv_full + sst, sph);
+                    if (lane == 0) tr.ev(44);
                     if (u > 0) mbar_wait(freeb + b, (u - 1) & 1);
+                    if (lane == 0) tr.ev(42);
                     tc_fence_after();
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
                     if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) MMA_SS(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
+                        tr.ev(43);
                         mma_commit(s_full + b);
                         if (sj == cnt - 1) mma_commit(q_empty + qb);
+                        tr.ev(41);
                     }
                     __syncwarp();
                     if (++sst == NST) { sst = 0; sph ^= 1; }
@@ -239,6 +252,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // ------------------------------------------------------------ P.V issuer: O += P_J V_J
         // (P from TMEM) as each P arrives.  A second issuing warp, so the tensor pipe is fed by
         // whichever stream is ready while the other waits (a commit stalls its issuing thread).
+        Tracer tr(p, 4);
         int pst = 0;
         uint32_t g = 0;
         for (int ks = 0;; ++ks) {
@@ -248,14 +262,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             for (int pj = 0; pj < cnt; ++pj) {
                 const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
                 mbar_wait(p_full + b, u & 1);
+                if (lane == 0) tr.ev(13);
                 tc_fence_after();
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + pst * STG + KV_BYTES));
                 if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < B / 16; ++k)
                         MMA_TS(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
+                    tr.ev(32);
                     mma_commit(freeb + b);
                     mma_commit(kv_empty + pst);  // S(pj) (K) completed before P(pj) existed
+                    tr.ev(33);
                 }
                 __syncwarp();
                 if (++pst == NST) pst = 0;
@@ -294,9 +311,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         uint32_t g = 0;
         int nq = 0;
         const float sl2 = p.scale_log2;
+        Tracer tr(p, threadIdx.x == 0 ? 2 : 3);
+        const bool trc = threadIdx.x == 0 || threadIdx.x == 64;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
+            if (trc) tr.ev(20);
             const int bh = h[1], t = h[2], cnt = h[3], rcnt = h[4 + slot];
             const int *msks = sc.msk + (ks & 3) * SCHED_CAP;
             const int row = t * 128 + r;
@@ -308,6 +328,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 const bool active = (msks[jj] >> slot) & 1;  // warp-uniform (B >= 32)
                 const uint32_t gs = g + jj, sb = gs % NBUF;
                 mbar_wait(s_full + sb, (gs / NBUF) & 1);
+                if (trc) tr.ev(21);
                 tc_fence_after();
                 uint32_t packed[B / 2];
                 float alpha = 1.f;
@@ -326,6 +347,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 #pragma unroll
                     for (int i = 4; i < B; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
                     float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                    if (trc) tr.ev(52);
                     mx *= sl2;  // scale > 0: max commutes with the scaling (log2 domain)
                     if (m_run == -INFINITY) {
                         m_run = mx;
@@ -336,18 +358,19 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     }
                     // packed fp32x2: s * scale*log2(e) - m for two columns per FFMA2; two running sums
                     const uint64_t sl22 = f2pack(sl2, sl2), nm2 = f2pack(-m_run, -m_run);
-                    uint64_t sum2 = 0ull;
+                    uint64_t sum2[2] = {0ull, 0ull};  // two independent FADD2 chains
 #pragma unroll
                     for (int i = 0; i < B; i += 2) {
                         float a0, a1;
                         f2unpack(ffma2(f2pack(s[i], s[i + 1]), sl22, nm2), a0, a1);
                         const float e0 = ex2m(a0, i), e1 = ex2m(a1, i + 1);
-                        sum2 = fadd2(sum2, f2pack(e0, e1));
+                        sum2[(i >> 1) & 1] = fadd2(sum2[(i >> 1) & 1], f2pack(e0, e1));
                         packed[i / 2] = pack_bf16(e0, e1);
                     }
                     float s0, s1;
-                    f2unpack(sum2, s0, s1);
+                    f2unpack(fadd2(sum2[0], sum2[1]), s0, s1);
                     l_run = l_run * alpha + (s0 + s1);
+                    if (trc) tr.ev(53);
                 } else {
 #pragma unroll
                     for (int i = 0; i < B / 2; ++i) packed[i] = 0u;
@@ -378,6 +401,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(p_full + sb);
+                if (trc) tr.ev(22);
             }
             // ---- epilogue: O / Z and lse (log2 domain internally)
             float f = 0.f, lse2;
@@ -401,6 +425,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     const uint32_t gp = g + pj;
                     mbar_wait(freeb + gp % NBUF, (gp / NBUF) & 1);
                 }
+                if (trc) tr.ev(23);
                 tc_fence_after();
                 // O / Z -> bf16 staged in this item's Q buffer (its last S is done), one TMA store
                 const int qb = nq & 1;
@@ -416,6 +441,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
                 mbar_arrive(staged + qb);
                 tc_fence_before();
+                if (trc) tr.ev(24);
             } else if (valid) {
                 zero_row_bf16(orow);
             }
@@ -830,6 +856,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
     constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
     constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;  // + 128 * accumulator pair
+    constexpr bool TSKV = Cfg<B>::DKV_TS;
+    constexpr uint32_t COL_KA = NBUF * BUFW + 128 * ACCB, COL_VA = COL_KA + 32;  // TSKV: K, V as A operands
     constexpr uint32_t TILE = B * 128;
     constexpr uint32_t STAGE = 2 * TILE + 1024;  // Q_I, dO_I, lse_I, D_I
     constexpr uint32_t IDESC_ST = idesc_bf16(128, B, false, false);   // S^T = K Q^T, dP^T = V dO^T
@@ -971,6 +999,14 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 ++nk;
                 const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
+                if (TSKV && elect_one()) {  // in issue order with the MMAs below (and the last item's)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        tmem_cp_128x256b(tmem + COL_KA + 8 * k, dK0 + 2 * k);
+                        tmem_cp_128x256b(tmem + COL_VA + 8 * k, dV0 + 2 * k);
+                    }
+                }
+                __syncwarp();
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
                     if (NSW > 1 && (int)b != sw) {
@@ -990,10 +1026,18 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
                     const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
                     if (elect_one()) {
+                        if (TSKV) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
+                            for (int k = 0; k < 4; ++k) MMA_TS(tmem + cs, tmem + COL_KA + 8 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
+                            for (int k = 0; k < 4; ++k)
+                                MMA_TS(tmem + cs + B, tmem + COL_VA + 8 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs, dK0 + 2 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) MMA_SS(tmem + cs + B, dV0 + 2 * k, ddO0 + 2 * k, IDESC_ST, k > 0);
+                        }
                         tr.ev(43);
                         mma_commit(s_full + 2 * b + (PP ? (sj & 1) : 0));
                         tr.ev(41);

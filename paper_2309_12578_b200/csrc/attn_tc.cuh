@@ -33,6 +33,12 @@
 #ifndef SPION_DQ_TS  // dQ pass: Q / dO of the item in tensor memory (TS score MMAs) where TMEM allows
 #define SPION_DQ_TS 1
 #endif
+#ifndef SPION_TRACE_EVENTS  // 1: per-role event traces of CTA 0 (tools/trace_*.py; costs issue slots)
+#define SPION_TRACE_EVENTS 0
+#endif
+#ifndef SPION_DKV_TS  // dK/dV pass: K / V of the item in tensor memory (TS score MMAs), NBUF 3 -> 2
+#define SPION_DKV_TS 0
+#endif
 #ifndef SPION_DBG_NOLOAD  // per-block operand tiles not loaded
 #define SPION_DBG_NOLOAD 0
 #endif
@@ -103,7 +109,7 @@ struct Tracer {
         if (p.trace && blockIdx.x == 0) base = p.trace + 16 + role * 2048;
     }
     __device__ __forceinline__ void ev(int id) {
-        if (base && n < 2048) {  // one 64-bit store: SM clock << 8 | event id
+        if (SPION_TRACE_EVENTS && base && n < 2048) {  // one 64-bit store: SM clock << 8 | event id
             base[n] = (unsigned long long)id | ((unsigned long long)clock64() << 8);
             ++n;
         }

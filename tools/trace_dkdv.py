@@ -1,4 +1,6 @@
 """Debug: event trace of CTA 0 of the dK/dV kernel (SPION_TRACE=1); each event = SM clock << 8 | id.
+Needs a build with the events compiled in: python tools/build_variant.py trev -DSPION_TRACE_EVENTS=1,
+then SPION_LIB=build_variants/trev/libspion.so python tools/trace_dkdv.py.
 
 roles: 0 producer, 1 S^T/dP^T MMA warp, 2/3 softmax thread 0 / 128, 4 dV/dK MMA warp.
 Prints the median cycles between consecutive events of each role, and a raw window."""
