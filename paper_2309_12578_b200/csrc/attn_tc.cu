@@ -91,6 +91,11 @@ template <int B> struct Cfg {
     // NST % NBUF == 0) stay in order within one warp, as mbarrier parity waits require
     static constexpr int DQ_NSW = DQ_CTAS == 1 && SPION_NSW ? DQ_NBUF : 1;
     static constexpr int DKV_NSW = 1;
+    // a dedicated epilogue warpgroup (dK/dV accumulators -> bf16 staging) where one CTA with two softmax
+    // warpgroups owns the SM, so the softmax warps run into the next item while an item's last dV/dK
+    // MMAs drain and its accumulators are read (512 threads, setmaxnreg budgets)
+    static constexpr bool DKV_EPI = SPION_DKV_EPI && DKV_CTAS == 1 && DKV_MW == 8 && DKV_NSW == 1;
+    static constexpr int DKV_THREADS = bwd_threads(DKV_MW, DKV_NSW) + (DKV_EPI ? 128 : 0);
     static_assert(FWD_NST >= FWD_NBUF && DQ_NST >= DQ_NBUF && DKV_NST >= DKV_NBUF, "ring shallower than look-ahead");
 };
 // ============================================================================ forward
@@ -124,6 +129,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     Sched sc = make_sched(sSched, kv_empty + NST);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
     uint64_t *staged = kv_empty + NST + 9;  // [2]: O of the item using Q buffer qb staged
+    // li: the P.V issuer has issued an item's last MMA (the S issuer starts the next item's MMAs
+    // behind it, so the item's accumulator completes without queueing behind look-ahead MMAs)
+    uint64_t *li = staged + 2;
+    uint64_t *o_empty = staged + 3;  // the (deferred) epilogue has read the O accumulator
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -133,6 +142,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         for (int i = 0; i < NBUF; ++i) { mbar_init(s_full + i, 1); mbar_init(p_full + i, 128); mbar_init(freeb + i, 1); }
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         for (int i = 0; i < 2; ++i) mbar_init(staged + i, 128);
+        mbar_init(li, 1);
+        mbar_init(o_empty, 128);
         sched_init(sc, 7);
         fence_barrier_init();
     }
@@ -222,6 +233,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 const int qb = nq & 1;
                 mbar_wait(q_full + qb, (nq >> 1) & 1);
                 if (lane == 0) tr.ev(11);
+                if (SPION_ITEM_FENCE && nq > 0) mbar_wait(li, (nq - 1) & 1);
                 tc_fence_after();
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
@@ -253,12 +265,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // (P from TMEM) as each P arrives.  A second issuing warp, so the tensor pipe is fed by
         // whichever stream is ready while the other waits (a commit stalls its issuing thread).
         Tracer tr(p, 4);
-        int pst = 0;
+        int pst = 0, no = 0;
         uint32_t g = 0;
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
             const int cnt = h[3];
+            if (SPION_DEFER_FWD && cnt > 0) {  // the previous item's (deferred) epilogue has read O
+                if (no > 0) mbar_wait(o_empty, (no - 1) & 1);
+                ++no;
+            }
             for (int pj = 0; pj < cnt; ++pj) {
                 const uint32_t gp = g + pj, b = gp % NBUF, u = gp / NBUF;
                 mbar_wait(p_full + b, u & 1);
@@ -270,6 +286,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     for (int k = 0; k < B / 16; ++k)
                         MMA_TS(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
                     tr.ev(32);
+                    if (SPION_ITEM_FENCE && pj == cnt - 1) mbar_arrive(li);
                     mma_commit(freeb + b);
                     mma_commit(kv_empty + pst);  // S(pj) (K) completed before P(pj) existed
                     tr.ev(33);
@@ -313,6 +330,38 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const float sl2 = p.scale_log2;
         Tracer tr(p, threadIdx.x == 0 ? 2 : 3);
         const bool trc = threadIdx.x == 0 || threadIdx.x == 64;
+        // pending epilogue (SPION_DEFER_FWD): O / Z of an item whose blocks are done, staged after the
+        // first block of the next item, so the softmax warps do not idle while its last P.V drains (the
+        // next item's first P.V waits for it through o_empty)
+        int dfr_qb = -1, dfr_cnt = 0;
+        uint32_t dfr_g = 0;
+        float dfr_f = 0.f;
+        auto epilogue = [&]() {
+            if (dfr_qb < 0) return;
+            // every P.V of the item that is not yet known complete (the last NBUF at most)
+            for (int pj = (dfr_cnt > NBUF ? dfr_cnt - NBUF : 0); pj < dfr_cnt; ++pj) {
+                const uint32_t gp = dfr_g + pj;
+                mbar_wait(freeb + gp % NBUF, (gp / NBUF) & 1);
+            }
+            if (trc) tr.ev(23);
+            tc_fence_after();
+            // O / Z -> bf16 staged in the item's Q buffer (its last S is done), one TMA store
+            uint8_t *sO = sQ + dfr_qb * 16384;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                float o[32];
+                tmem_ld32(tl + COL_O + hh * 32, o);
+                tmem_ld_wait();
+                stage_row_bf16(sO, r, o, dfr_f, hh);
+            }
+            tc_fence_before();
+            if (SPION_DEFER_FWD) mbar_arrive(o_empty);
+            fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
+            mbar_arrive(staged + dfr_qb);
+            tc_fence_before();
+            if (trc) tr.ev(24);
+            dfr_qb = -1;
+        };
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -402,7 +451,9 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tc_fence_before();
                 mbar_arrive(p_full + sb);
                 if (trc) tr.ev(22);
+                if (jj == 0) epilogue();  // the previous item's (deferred), after this item's first block
             }
+            epilogue();  // (an item without blocks)
             // ---- epilogue: O / Z and lse (log2 domain internally)
             float f = 0.f, lse2;
             const int64_t ecnt = (int64_t)B * rcnt;
@@ -420,28 +471,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 f = exp2f(m_run - lse2);
             }
             if (cnt > 0) {
-                // every P.V of the item that is not yet known complete (the last NBUF at most)
-                for (int pj = (cnt > NBUF ? cnt - NBUF : 0); pj < cnt; ++pj) {
-                    const uint32_t gp = g + pj;
-                    mbar_wait(freeb + gp % NBUF, (gp / NBUF) & 1);
-                }
-                if (trc) tr.ev(23);
-                tc_fence_after();
-                // O / Z -> bf16 staged in this item's Q buffer (its last S is done), one TMA store
-                const int qb = nq & 1;
+                dfr_qb = nq & 1;
                 ++nq;
-                uint8_t *sO = sQ + qb * 16384;
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    float o[32];
-                    tmem_ld32(tl + COL_O + hh * 32, o);
-                    tmem_ld_wait();
-                    stage_row_bf16(sO, r, o, f, hh);
-                }
-                fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
-                mbar_arrive(staged + qb);
-                tc_fence_before();
-                if (trc) tr.ev(24);
+                dfr_cnt = cnt;
+                dfr_g = g;
+                dfr_f = f;
+                if (!SPION_DEFER_FWD) epilogue();
             } else if (valid) {
                 zero_row_bf16(orow);
             }
@@ -449,6 +484,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             g += cnt;
             sched_release(sc, ks, true);
         }
+        epilogue();  // the last item's
     }
     __syncthreads();
     sched_finish(p, t_start);
@@ -495,6 +531,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_empty + NST + 8);
     uint64_t *staged = kv_empty + NST + 9;  // [2]: dQ of the item using Q buffer qb staged
     uint64_t *acc_empty = staged + 2;       // the epilogue has read the dQ accumulator
+    uint64_t *li = acc_empty + 1;           // the dQ issuer has issued an item's last MMA (as forward)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -511,6 +548,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         for (int i = 0; i < NST; ++i) { mbar_init(kv_full + i, 1); mbar_init(kv_empty + i, 1); }
         for (int i = 0; i < 2; ++i) mbar_init(staged + i, 32 * MW);
         mbar_init(acc_empty, 32 * MW);
+        mbar_init(li, 1);
         sched_init(sc, 2 + NSW + MW);
         fence_barrier_init();
     }
@@ -611,6 +649,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             if (cnt > 0) {
                 const int qb = nq & 1;
                 mbar_wait(q_full + qb, (nq >> 1) & 1);
+                if (SPION_ITEM_FENCE && NSW == 1 && nq > 0) mbar_wait(li, (nq - 1) & 1);
                 tc_fence_after();
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
@@ -683,6 +722,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         for (int k = 0; k < B / 16; ++k)
                             MMA_TS(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
                                         (pj > 0) || (k > 0));
+                        if (SPION_ITEM_FENCE && NSW == 1 && pj == cnt - 1) mbar_arrive(li);
                         mma_commit(freeb + b);
                         mma_commit(kv_empty + pst);
                         if (pj == cnt - 1) mma_commit(dq_full);
@@ -725,6 +765,32 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
         uint32_t dq_ph = 0, g = 0, sph = 0;  // sph: phase bit per score buffer (this warpgroup's uses)
         int nq = 0;
         const float sl2 = p.scale_log2;
+        // pending epilogue (SPION_DEFER_DQ): the Q buffer of an item whose blocks are done; run after this
+        // warpgroup's first block of the next item, so the softmax warps do not idle while the item's last
+        // dQ MMAs drain (the next item's first dQ MMA waits for it through acc_empty)
+        int dfr_qb = -1;
+        auto epilogue = [&]() {
+            if (dfr_qb < 0) return;
+            mbar_wait(dq_full, dq_ph);
+            dq_ph ^= 1;
+            tc_fence_after();
+            // dQ -> bf16 staged in the item's Q buffer (every MMA of the item is done), one TMA store
+            uint8_t *sdQ = sQ + dfr_qb * 16384;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (MW == 8 && hh != wg) continue;  // two warpgroups: one 32-column half each
+                float v[32];
+                tmem_ld32(tl + COL_DQ + hh * 32, v);
+                tmem_ld_wait();
+                stage_row_bf16(sdQ, r, v, p.scale, hh);
+            }
+            tc_fence_before();
+            mbar_arrive(acc_empty);  // the next item's first dQ MMA may overwrite the accumulator
+            fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
+            mbar_arrive(staged + dfr_qb);
+            tc_fence_before();
+            dfr_qb = -1;
+        };
         for (int ks = 0;; ++ks) {
             const int *h = sched_wait(sc, ks);
             if (h[0] < 0) break;
@@ -808,28 +874,15 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(ds_full + sb);
+                epilogue();  // the previous item's (deferred), after this item's first block
             }
-            mbar_wait(dq_full, dq_ph);
-            dq_ph ^= 1;
-            tc_fence_after();
-            // dQ -> bf16 staged in this item's Q buffer (every MMA of the item is done), one TMA store
-            uint8_t *sdQ = sQ + qb * 16384;
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                if (MW == 8 && hh != wg) continue;  // two warpgroups: one 32-column half each
-                float v[32];
-                tmem_ld32(tl + COL_DQ + hh * 32, v);
-                tmem_ld_wait();
-                stage_row_bf16(sdQ, r, v, p.scale, hh);
-            }
-            tc_fence_before();
-            mbar_arrive(acc_empty);  // the next item's first dQ MMA may overwrite the accumulator
-            fence_proxy_async_smem();  // generic-proxy writes -> the TMA store (async proxy)
-            mbar_arrive(staged + qb);
-            tc_fence_before();
+            epilogue();  // (no block of this warpgroup in this item)
+            dfr_qb = qb;
+            if (!SPION_DEFER_DQ) epilogue();
             g += cnt;
             sched_release(sc, ks, true);
         }
+        epilogue();  // the last item's
     }
     __syncthreads();
     sched_finish(p, t_start);
@@ -845,7 +898,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
 // blocks ahead of the softmax warps); P^T, dS^T packed over them feed dV += P^T dO_I,
 // dK += dS^T Q_I as A operands from tensor memory.
 template <int B>
-__global__ void __launch_bounds__(bwd_threads(Cfg<B>::DKV_MW, Cfg<B>::DKV_NSW), Cfg<B>::DKV_CTAS)
+__global__ void __launch_bounds__(Cfg<B>::DKV_THREADS, Cfg<B>::DKV_CTAS)
 attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcParams p) {
@@ -854,6 +907,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     constexpr bool PP = MW == 8 && Cfg<B>::PING;   // warpgroups take alternate blocks
     constexpr int CPT = PP || MW == 4 ? B : B / 2;  // columns of a block per softmax thread
     constexpr int W_PROD = MW, W_MMA = MW + 1, W_STORE = MW + 2, W_MMA2 = MW + 3, W_MMA3 = MW + 4;
+    constexpr bool EPI = Cfg<B>::DKV_EPI;
+    constexpr int W_EPI = MW + 3 + NSW;  // EPI: warps W_EPI .. W_EPI + 3 (TMEM lane quarters 0..3)
+    constexpr int NEPI = EPI ? 128 : 32 * MW;  // threads that read the accumulators and stage dK/dV
     constexpr uint32_t BUFW = 2 * B;  // S^T at b*BUFW, dP^T at b*BUFW + B
     constexpr uint32_t COL_DK = NBUF * BUFW, COL_DV = NBUF * BUFW + 64;  // + 128 * accumulator pair
     constexpr bool TSKV = Cfg<B>::DKV_TS;
@@ -875,6 +931,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_empty + NST + 8);
     uint64_t *staged = q_empty + NST + 9;  // [KVB]: dK/dV of the item using K/V buffer kb staged there
     uint64_t *acc_empty = staged + 3;      // [ACCB]: the epilogue has read accumulator pair a
+    uint64_t *li = acc_empty + 2;          // the dV/dK issuer has issued an item's last MMAs (as forward)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -885,10 +942,11 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         // per (buffer, consumer), so each has one in-order producer and one in-order consumer
         for (int i = 0; i < 2 * NBUF; ++i) mbar_init(s_full + i, 1);
         for (int i = 0; i < NBUF; ++i) { mbar_init(p_full + i, PP ? 128 : 32 * MW); mbar_init(freeb + i, 1); }
-        for (int i = 0; i < ACCB; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, 32 * MW); }
+        for (int i = 0; i < ACCB; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, NEPI); }
         for (int i = 0; i < NST; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        for (int i = 0; i < KVB; ++i) mbar_init(staged + i, 32 * MW);
-        sched_init(sc, 2 + NSW + MW);
+        for (int i = 0; i < KVB; ++i) mbar_init(staged + i, NEPI);
+        mbar_init(li, 1);
+        sched_init(sc, 2 + NSW + MW + (EPI ? 4 : 0));
         fence_barrier_init();
     }
     if (warp == W_MMA) tmem_alloc<Cfg<B>::DKV_COLS>(tmem_slot);
@@ -899,7 +957,10 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
     const uint32_t tmem = *tmem_slot;
     const unsigned long long t_start = p.trace ? gtimer() : 0ull;
     const int nitems = (int)(p.bh * p.ntiles);
-
+    // EPI: register budgets per warpgroup (one setmaxnreg at the top of each warpgroup's branch):
+    // softmax 2 x 128 x 168 + single-lane roles 128 x 64 + epilogue 128 x 96 <= 65536
+    if (warp >= W_PROD && (!EPI || warp < W_EPI)) {
+    if (EPI) regs_dec<64>();
     if (warp == W_PROD) {
         Tracer tr(p, 0);
         if (lane == 0) {
@@ -979,7 +1040,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             issued = nissued;
             item = nitem;
         }
-    } else if (warp == W_MMA || warp >= W_MMA3) {
+    } else if (warp == W_MMA || (warp >= W_MMA3 && warp < W_EPI)) {
         // S^T / dP^T issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
         // with NSW = NBUF, warp sw issues the blocks whose score buffer is sw
         const int sw = warp == W_MMA ? 0 : warp - W_MMA3 + 1;
@@ -995,6 +1056,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 const int kb = nk % KVB;
                 mbar_wait(kv_full + kb, (nk / KVB) & 1);
                 if (lane == 0) tr.ev(11);
+                if (SPION_ITEM_FENCE && NSW == 1 && nk > 0) mbar_wait(li, (nk - 1) & 1);
                 tc_fence_after();
                 ++nk;
                 const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
@@ -1089,6 +1151,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                             MMA_TS(tmem + cdk, tmem + cs + B + 32 * (k / 2) + 8 * (k % 2), dQ0 + 128 * k, IDESC_DKV,
                                         (pj > 0) || (k > 0));
                         tr.ev(32);
+                        if (SPION_ITEM_FENCE && NSW == 1 && pj == cnt - 1) mbar_arrive(li);
                         mma_commit(freeb + b);
                         mma_commit(q_empty + pst);
                         if (pj == cnt - 1) mma_commit(acc_full + ab);
@@ -1131,7 +1194,43 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             sched_release(sc, ks, true);
         }
         if (lane == 0) bulk_wait0();
+    }
+    } else if (EPI && warp >= W_EPI) {
+        regs_dec<96>();
+        // ------------------------------------------------------------ epilogue warpgroup: per item,
+        // once its last dV/dK MMAs are done, dK * scale and dV -> bf16 staged in the item's K/V buffer
+        const int r = (warp & 3) * 32 + lane;  // key row of the tile = TMEM lane
+        const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        int nk = 0, na = 0;
+        for (int ks = 0;; ++ks) {
+            const int *h = sched_wait(sc, ks);
+            if (h[0] < 0) break;
+            if (h[3] > 0) {
+                const int kb = nk % KVB, ab = na % ACCB;
+                mbar_wait(acc_full + ab, (uint32_t)(na / ACCB) & 1);
+                tc_fence_after();
+                uint8_t *sdK = sKV + kb * 32768, *sdV = sdK + 16384;
+                const uint32_t cdk = COL_DK + 128 * ab, cdv = COL_DV + 128 * ab;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    float kv[32], vv[32];
+                    tmem_ld32(tl + cdk + hh * 32, kv);
+                    tmem_ld32(tl + cdv + hh * 32, vv);
+                    tmem_ld_wait();
+                    stage_row_bf16(sdK, r, kv, p.scale, hh);
+                    stage_row_bf16(sdV, r, vv, 1.f, hh);
+                }
+                tc_fence_before();
+                mbar_arrive(acc_empty + ab);  // a later item's first dV/dK MMAs may overwrite the pair
+                fence_proxy_async_smem();     // generic-proxy writes -> the TMA store (async proxy)
+                mbar_arrive(staged + kb);
+                ++nk;
+                ++na;
+            }
+            sched_release(sc, ks, true);
+        }
     } else {
+        if (EPI) regs_inc<168>();
         const int r = (warp & 3) * 32 + lane;  // key row of the tile = TMEM lane
         const int wg = warp >> 2;              // warpgroup: alternate blocks (MW = 8); epilogue halves
         const int slot = r / B;
@@ -1145,7 +1244,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
         int dfr_kb = -1, dfr_ab = 0;
         uint32_t dfr_par = 0;
         auto epilogue = [&]() {
-            if (dfr_kb < 0) return;
+            if (EPI || dfr_kb < 0) return;
             mbar_wait(acc_full + dfr_ab, dfr_par);
             if (trc) tr.ev(23);
             tc_fence_after();
@@ -1273,7 +1372,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             dfr_par = (uint32_t)(na / ACCB) & 1;
             ++nk;
             ++na;
-            if (ACCB == 1) epilogue();
+            if (ACCB == 1 && !SPION_DEFER_DKV) epilogue();
             g += cnt;
             sched_release(sc, ks, true);
         }
@@ -1477,7 +1576,7 @@ static spion_status bwd_tc_t(const AttnArgs &a, cudaStream_t s) {
     q.D = const_cast<float *>(a.D);
     q.dK = a.dK;
     q.dV = a.dV;
-    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), bwd_threads(Cfg<B>::DKV_MW, Cfg<B>::DKV_NSW), dkv_smem<B>(), s>>>(
+    attn_bwd_dkdv_tc_kernel<B><<<grid_for(q, Cfg<B>::DKV_CTAS), Cfg<B>::DKV_THREADS, dkv_smem<B>(), s>>>(
         mkB, mvB, mqB, mdoB, mdkB, mdvB, q);
     SPION_LAUNCH_CHECK();
     note_tc_launch(2);

@@ -36,6 +36,21 @@
 #ifndef SPION_TRACE_EVENTS  // 1: per-role event traces of CTA 0 (tools/trace_*.py; costs issue slots)
 #define SPION_TRACE_EVENTS 0
 #endif
+#ifndef SPION_ITEM_FENCE  // the score-MMA issuer starts an item's MMAs only after the previous item's last
+#define SPION_ITEM_FENCE 0  // accumulating MMAs were issued (tensor-pipe order: the accumulator finishes first)
+#endif
+#ifndef SPION_DEFER_DKV  // item epilogues run after the softmax warps' first block of the next item
+#define SPION_DEFER_DKV 0
+#endif
+#ifndef SPION_DEFER_DQ
+#define SPION_DEFER_DQ 0
+#endif
+#ifndef SPION_DEFER_FWD
+#define SPION_DEFER_FWD 0
+#endif
+#ifndef SPION_DKV_EPI  // dK/dV pass: a dedicated epilogue warpgroup (B = 64)
+#define SPION_DKV_EPI 0
+#endif
 #ifndef SPION_DKV_TS  // dK/dV pass: K / V of the item in tensor memory (TS score MMAs), NBUF 3 -> 2
 #define SPION_DKV_TS 0
 #endif
