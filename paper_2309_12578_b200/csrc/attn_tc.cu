@@ -180,7 +180,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             }
             if (elect_one()) {
                 mbar_arrive_expect_tx(q_full + qb, 16384);
-                tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, h[2] * 128, h[1]);
+                tma_ld(sQ + qb * 16384, &tmQ, q_full + qb, 0, h[2] * 128, h[1], l2_evict_first());
             }
             __syncwarp();
             ++nq;
@@ -207,8 +207,9 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         mbar_arrive(kv_full + st);
                     } else {
                         mbar_arrive_expect_tx(kv_full + st, STG);
-                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                        const uint64_t keep = l2_evict_last();  // K_J, V_J: read by every tile listing J
+                        tma_ld(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh, keep);
+                        tma_ld(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh, keep);
                     }
                 }
                 __syncwarp();
@@ -310,7 +311,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 mbar_wait(staged + sb, (ns >> 1) & 1);
                 ++ns;
                 if (lane == 0) {
-                    tma_store_3d(&tmO, sQ + sb * 16384, 0, t * 128, bh);
+                    tma_st(&tmO, sQ + sb * 16384, 0, t * 128, bh, l2_evict_first());
                     bulk_commit();
                     bulk_wait_read0();
                     mbar_arrive(q_empty + sb);
@@ -586,8 +587,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 }
                 if (elect_one()) {
                     mbar_arrive_expect_tx(q_full + qb, 32768);
-                    tma_load_3d(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh);
-                    tma_load_3d(sdO + qb * 16384, &tmdO, q_full + qb, 0, t * 128, bh);
+                    const uint64_t once = l2_evict_first();  // the item's own rows
+                    tma_ld(sQ + qb * 16384, &tmQ, q_full + qb, 0, t * 128, bh, once);
+                    tma_ld(sdO + qb * 16384, &tmdO, q_full + qb, 0, t * 128, bh, once);
                 }
                 __syncwarp();
                 tstate = 1;
@@ -598,7 +600,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             }
             if (elect_one()) {
                 mbar_arrive_expect_tx(o_full, 16384);
-                tma_load_3d(sO, &tmO, o_full, 0, t * 128, bh);
+                tma_ld(sO, &tmO, o_full, 0, t * 128, bh, l2_evict_first());
             }
             __syncwarp();
             tstate = 0;
@@ -625,8 +627,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         mbar_arrive(kv_full + st);
                     } else {
                         mbar_arrive_expect_tx(kv_full + st, STG);
-                        tma_load_3d(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh);
-                        tma_load_3d(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh);
+                        const uint64_t keep = l2_evict_last();  // K_J, V_J: read by every tile listing J
+                        tma_ld(sKV + st * STG, &tmK, kv_full + st, 0, col[j] * B, bh, keep);
+                        tma_ld(sKV + st * STG + KV_BYTES, &tmV, kv_full + st, 0, col[j] * B, bh, keep);
                     }
                 }
                 __syncwarp();
@@ -747,7 +750,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 mbar_wait(staged + sb, (ns >> 1) & 1);
                 ++ns;
                 if (lane == 0) {
-                    tma_store_3d(&tmdQ, sQ + sb * 16384, 0, t * 128, bh);
+                    tma_st(&tmdQ, sQ + sb * 16384, 0, t * 128, bh, l2_evict_first());
                     bulk_commit();
                     bulk_wait_read0();
                     mbar_arrive(q_empty + sb);
@@ -995,8 +998,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 for (int sl = 0; sl < p.S; ++sl) {
                     const int c = pm[sl];
                     if (c >= p.n) continue;
-                    tma_load_3d(sKV + kb * 32768 + sl * B * 128, &tmK, kv_full + kb, 0, c * B, bh);
-                    tma_load_3d(sKV + kb * 32768 + 16384 + sl * B * 128, &tmV, kv_full + kb, 0, c * B, bh);
+                    const uint64_t once = l2_evict_first();  // the item's own key rows
+                    tma_ld(sKV + kb * 32768 + sl * B * 128, &tmK, kv_full + kb, 0, c * B, bh, once);
+                    tma_ld(sKV + kb * 32768 + 16384 + sl * B * 128, &tmV, kv_full + kb, 0, c * B, bh, once);
                 }
             }
             __syncwarp();
@@ -1027,8 +1031,9 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         mbar_arrive(q_full + st);
                     } else {
                         mbar_arrive_expect_tx(q_full + st, 2 * TILE + 2 * B * 4);
-                        tma_load_3d(stg, &tmQ, q_full + st, 0, I * B, bh);
-                        tma_load_3d(stg + TILE, &tmdO, q_full + st, 0, I * B, bh);
+                        const uint64_t keep = l2_evict_last();  // Q_I, dO_I: read by every tile listing I
+                        tma_ld(stg, &tmQ, q_full + st, 0, I * B, bh, keep);
+                        tma_ld(stg + TILE, &tmdO, q_full + st, 0, I * B, bh, keep);
                         bulk_load(stg + 2 * TILE, p.lse + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
                         bulk_load(stg + 2 * TILE + 512, p.D + (int64_t)bh * p.L + (int64_t)I * B, B * 4, q_full + st);
                     }
@@ -1182,8 +1187,8 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     for (int sl = 0; sl < p.S; ++sl) {
                         const int c = pm[sl];
                         if (c >= p.n) continue;
-                        tma_store_3d(&tmdK, sKV + sb * 32768 + sl * B * 128, 0, c * B, bh);
-                        tma_store_3d(&tmdV, sKV + sb * 32768 + 16384 + sl * B * 128, 0, c * B, bh);
+                        tma_st(&tmdK, sKV + sb * 32768 + sl * B * 128, 0, c * B, bh, l2_evict_first());
+                        tma_st(&tmdV, sKV + sb * 32768 + 16384 + sl * B * 128, 0, c * B, bh, l2_evict_first());
                     }
                     bulk_commit();
                     bulk_wait_read0();

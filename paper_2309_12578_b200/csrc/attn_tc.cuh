@@ -51,6 +51,9 @@
 #ifndef SPION_DKV_EPI  // dK/dV pass: a dedicated epilogue warpgroup (B = 64)
 #define SPION_DKV_EPI 0
 #endif
+#ifndef SPION_L2HINT  // TMA copies carry L2 eviction priorities (read-once tiles first, gathered blocks last)
+#define SPION_L2HINT 1
+#endif
 #ifndef SPION_DKV_TS  // dK/dV pass: K / V of the item in tensor memory (TS score MMAs), NBUF 3 -> 2
 #define SPION_DKV_TS 0
 #endif
@@ -88,6 +91,15 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 // element i of an unrolled row loop: SPION_POLY of every 16 on the FMA pipe, the rest on the SFU
 __device__ __forceinline__ float ex2m(float x, int i) { return (i & 15) < SPION_POLY ? ex2_poly(x) : ex2(x); }
+// TMA copies with an L2 eviction priority (SPION_L2HINT; plain copies otherwise)
+__device__ __forceinline__ void tma_ld(void *dst, const void *tmap, uint64_t *bar, int c0, int c1, int c2, uint64_t pol) {
+    if (SPION_L2HINT) tma_load_3d_hint(dst, tmap, bar, c0, c1, c2, pol);
+    else tma_load_3d(dst, tmap, bar, c0, c1, c2);
+}
+__device__ __forceinline__ void tma_st(const void *tmap, const void *src, int c0, int c1, int c2, uint64_t pol) {
+    if (SPION_L2HINT) tma_store_3d_hint(tmap, src, c0, c1, c2, pol);
+    else tma_store_3d(tmap, src, c0, c1, c2);
+}
 static constexpr float LOG2E = 1.4426950408889634f;
 static constexpr float LN2 = 0.6931471805599453f;
 
