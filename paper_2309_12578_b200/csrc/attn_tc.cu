@@ -220,6 +220,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             item = nitem;
         }
     } else if (warp == W_MMA) {
+        if (!SPION_LANE0 || lane == 0) {  // SPION_LANE0: the issuing role runs on one thread
         // ------------------------------------------------------------ S issuer (converged warp,
         // one elected lane issues): S = Q K_J^T up to NBUF blocks ahead of the softmax
         Tracer tr(p, 1);
@@ -246,7 +247,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     if (lane == 0) tr.ev(42);
                     tc_fence_after();
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
-                    if (elect_one()) {
+                    if (ISSUER()) {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) MMA_SS(tmem + b * B, dQ0 + 2 * k, dK0 + 2 * k, IDESC_S, k > 0);
                         tr.ev(43);
@@ -254,14 +255,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         if (sj == cnt - 1) mma_commit(q_empty + qb);
                         tr.ev(41);
                     }
-                    __syncwarp();
+                    ROLE_SYNC();
                     if (++sst == NST) { sst = 0; sph ^= 1; }
                 }
                 g += cnt;
             }
-            sched_release(sc, ks, true);
+            sched_release(sc, ks, !SPION_LANE0);
+        }
         }
     } else if (warp == W_MMA2) {
+        if (!SPION_LANE0 || lane == 0) {  // SPION_LANE0: the issuing role runs on one thread
         // ------------------------------------------------------------ P.V issuer: O += P_J V_J
         // (P from TMEM) as each P arrives.  A second issuing warp, so the tensor pipe is fed by
         // whichever stream is ready while the other waits (a commit stalls its issuing thread).
@@ -282,7 +285,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 if (lane == 0) tr.ev(13);
                 tc_fence_after();
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + pst * STG + KV_BYTES));
-                if (elect_one()) {
+                if (ISSUER()) {
 #pragma unroll
                     for (int k = 0; k < B / 16; ++k)
                         MMA_TS(tmem + COL_O, tmem + b * B + 8 * k, dV0 + 128 * k, IDESC_PV, (pj > 0) || (k > 0));
@@ -292,11 +295,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     mma_commit(kv_empty + pst);  // S(pj) (K) completed before P(pj) existed
                     tr.ev(33);
                 }
-                __syncwarp();
+                ROLE_SYNC();
                 if (++pst == NST) pst = 0;
             }
             g += cnt;
-            sched_release(sc, ks, true);
+            sched_release(sc, ks, !SPION_LANE0);
+        }
         }
     } else if (warp == W_STORE) {
         // storer: once the softmax warps have staged an item's output tile(s) in shared
@@ -640,6 +644,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             item = nitem;
         }
     } else if (warp == W_MMA || warp >= W_MMA3) {
+        if (!SPION_LANE0 || lane == 0) {  // SPION_LANE0: the issuing role runs on one thread
         // S / dP issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
         // with NSW = NBUF, warp sw issues the blocks whose score buffer is sw
         const int sw = warp == W_MMA ? 0 : warp - W_MMA3 + 1;
@@ -657,14 +662,14 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                 ++nq;
                 const uint64_t dQ0 = sdesc_sw128(smem_u32(sQ + qb * 16384));
                 const uint64_t ddO0 = sdesc_sw128(smem_u32(sdO + qb * 16384));
-                if (TSQ && elect_one()) {  // in issue order with the MMAs below (and the last item's)
+                if (TSQ && ISSUER()) {  // in issue order with the MMAs below (and the last item's)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         tmem_cp_128x256b(tmem + COL_QA + 8 * k, dQ0 + 2 * k);
                         tmem_cp_128x256b(tmem + COL_DOA + 8 * k, ddO0 + 2 * k);
                     }
                 }
-                __syncwarp();
+                ROLE_SYNC();
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
                     if (NSW > 1 && (int)b != sw) {
@@ -679,7 +684,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                     const uint32_t cs = b * BUFW;
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + sst * STG));
                     const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + sst * STG + KV_BYTES));
-                    if (elect_one()) {
+                    if (ISSUER()) {
                         if (TSQ) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) MMA_TS(tmem + cs, tmem + COL_QA + 8 * k, dK0 + 2 * k, IDESC_S, k > 0);
@@ -694,16 +699,18 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         }
                         mma_commit(s_full + 2 * b + (PP ? (sj & 1) : 0));
                     }
-                    __syncwarp();
+                    ROLE_SYNC();
                     if (++sst == NST) { sst = 0; sph ^= 1; }
                 }
-                if (elect_one()) mma_commit(q_empty + qb);  // Q, dO no longer read by this warp's MMAs
-                __syncwarp();
+                if (ISSUER()) mma_commit(q_empty + qb);  // Q, dO no longer read by this warp's MMAs
+                ROLE_SYNC();
                 g += cnt;
             }
-            sched_release(sc, ks, true);
+            sched_release(sc, ks, !SPION_LANE0);
+        }
         }
     } else if (warp == W_MMA2) {
+        if (!SPION_LANE0 || lane == 0) {  // SPION_LANE0: the issuing role runs on one thread
         // dQ issuer: dQ += dS_J K_J (dS from TMEM) as each dS arrives; a second issuing warp so
         // the tensor pipe is fed while the other waits (a commit stalls its issuing thread)
         int pst = 0, na = 0;
@@ -720,7 +727,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                     mbar_wait(ds_full + b, u & 1);
                     tc_fence_after();
                     const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + pst * STG));
-                    if (elect_one()) {
+                    if (ISSUER()) {
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
                             MMA_TS(tmem + COL_DQ, tmem + b * BUFW + 32 * (k / 2) + 8 * (k % 2), dK0 + 128 * k, IDESC_DQ,
@@ -730,12 +737,13 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
                         mma_commit(kv_empty + pst);
                         if (pj == cnt - 1) mma_commit(dq_full);
                     }
-                    __syncwarp();
+                    ROLE_SYNC();
                     if (++pst == NST) pst = 0;
                 }
                 g += cnt;
             }
-            sched_release(sc, ks, true);
+            sched_release(sc, ks, !SPION_LANE0);
+        }
         }
     } else if (warp == W_STORE) {
         // storer: once the softmax warps have staged an item's output tile(s) in shared
@@ -1046,6 +1054,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
             item = nitem;
         }
     } else if (warp == W_MMA || (warp >= W_MMA3 && warp < W_EPI)) {
+        if (!SPION_LANE0 || lane == 0) {  // SPION_LANE0: the issuing role runs on one thread
         // S^T / dP^T issuers (converged warps, one elected lane issues), up to NBUF blocks ahead;
         // with NSW = NBUF, warp sw issues the blocks whose score buffer is sw
         const int sw = warp == W_MMA ? 0 : warp - W_MMA3 + 1;
@@ -1066,14 +1075,14 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                 ++nk;
                 const uint64_t dK0 = sdesc_sw128(smem_u32(sKV + kb * 32768));
                 const uint64_t dV0 = sdesc_sw128(smem_u32(sKV + kb * 32768 + 16384));
-                if (TSKV && elect_one()) {  // in issue order with the MMAs below (and the last item's)
+                if (TSKV && ISSUER()) {  // in issue order with the MMAs below (and the last item's)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         tmem_cp_128x256b(tmem + COL_KA + 8 * k, dK0 + 2 * k);
                         tmem_cp_128x256b(tmem + COL_VA + 8 * k, dV0 + 2 * k);
                     }
                 }
-                __syncwarp();
+                ROLE_SYNC();
                 for (int sj = 0; sj < cnt; ++sj) {
                     const uint32_t gs = g + sj, b = gs % NBUF, u = gs / NBUF;
                     if (NSW > 1 && (int)b != sw) {
@@ -1092,7 +1101,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     const uint32_t cs = b * BUFW;
                     const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
                     const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
-                    if (elect_one()) {
+                    if (ISSUER()) {
                         if (TSKV) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) MMA_TS(tmem + cs, tmem + COL_KA + 8 * k, dQ0 + 2 * k, IDESC_ST, k > 0);
@@ -1109,18 +1118,20 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         mma_commit(s_full + 2 * b + (PP ? (sj & 1) : 0));
                         tr.ev(41);
                     }
-                    __syncwarp();
+                    ROLE_SYNC();
                     if (lane == 0) tr.ev(14);
                     if (++sst == NST) { sst = 0; sph ^= 1; }
                 }
                 // K/V no longer read by this warp's MMAs of the item (the same lane issued them)
-                if (elect_one()) mma_commit(kv_empty + kb);
-                __syncwarp();
+                if (ISSUER()) mma_commit(kv_empty + kb);
+                ROLE_SYNC();
                 g += cnt;
             }
-            sched_release(sc, ks, true);
+            sched_release(sc, ks, !SPION_LANE0);
+        }
         }
     } else if (warp == W_MMA2) {
+        if (!SPION_LANE0 || lane == 0) {  // SPION_LANE0: the issuing role runs on one thread
         // dV / dK issuer: dV += P^T dO_I, dK += dS^T Q_I (A from TMEM) as each block's P^T / dS^T
         // arrives; a second issuing warp so the tensor pipe is fed while the other waits
         Tracer tr(p, 4);
@@ -1145,7 +1156,7 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                     const uint64_t dQ0 = sdesc_sw128(smem_u32(stg));
                     const uint64_t ddO0 = sdesc_sw128(smem_u32(stg + TILE));
                     const uint32_t cs = b * BUFW;
-                    if (elect_one()) {
+                    if (ISSUER()) {
                         tr.ev(31);
 #pragma unroll
                         for (int k = 0; k < B / 16; ++k)
@@ -1162,13 +1173,14 @@ attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_co
                         if (pj == cnt - 1) mma_commit(acc_full + ab);
                         tr.ev(33);
                     }
-                    __syncwarp();
+                    ROLE_SYNC();
                     if (lane == 0) tr.ev(15);
                     if (++pst == NST) pst = 0;
                 }
                 g += cnt;
             }
-            sched_release(sc, ks, true);
+            sched_release(sc, ks, !SPION_LANE0);
+        }
         }
     } else if (warp == W_STORE) {
         // storer: once the softmax warps have staged an item's output tile(s) in shared

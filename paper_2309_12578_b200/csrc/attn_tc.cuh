@@ -54,6 +54,14 @@
 #ifndef SPION_L2HINT  // TMA copies carry L2 eviction priorities (read-once tiles first, gathered blocks last)
 #define SPION_L2HINT 1
 #endif
+#ifndef SPION_LANE0  // the MMA-issuing roles run on one thread (lane 0) instead of a converged warp
+#define SPION_LANE0 0
+#endif
+#define ISSUER() (SPION_LANE0 ? true : elect_one())
+#define ROLE_SYNC()                   \
+    do {                              \
+        if (!SPION_LANE0) __syncwarp(); \
+    } while (0)
 #ifndef SPION_DKV_TS  // dK/dV pass: K / V of the item in tensor memory (TS score MMAs), NBUF 3 -> 2
 #define SPION_DKV_TS 0
 #endif
