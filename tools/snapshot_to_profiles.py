@@ -21,8 +21,8 @@ def run(*a):
 old = open(os.path.join(dst, "ncu_summary.md")).read() if os.path.exists(os.path.join(dst, "ncu_summary.md")) else ""
 micro = old[old.index("## Microbenchmarks"):] if "## Microbenchmarks" in old else ""
 nv = open(os.path.join(src, "nvsmi.txt")).read().strip() if os.path.exists(os.path.join(src, "nvsmi.txt")) else ""
-out = [f"# ncu summaries, round 1 (snapshot `{os.path.basename(src)}`)\n",
-       "`tools/gpu_snapshot.sh` on one B200; `ncu --set full --clock-control none` (cold-cache, serialised",
+out = [f"# ncu summaries, {os.path.basename(os.path.normpath(dst))} (snapshot `{os.path.basename(src)}`)\n",
+       "`tools/gpu_r2.sh` (or `gpu_snapshot.sh`) on one B200; `ncu --set full --clock-control none` (cold-cache, serialised",
        "replays: compare shares, not absolutes). Bench lines of the same build: `bench_*.json`; DRAM traffic",
        "per call: `ncu_traffic.json` (the backward reads more than its algorithmic bytes because the dQ and",
        "dK/dV kernels both read Q, K, V and dO).", "", "```", nv, "```", ""]
