@@ -81,7 +81,8 @@ def config_dict(cfg, args, world):
         "batch": cfg["batch"], "towers": cfg["towers"], "bh": bh, "filter": FILTER, "alpha": args.alpha,
         "softmax": args.mode, "step": "pattern(scores)+attn_fwd+attn_bwd",
         "pipeline": "sequential" if args.no_pipeline else "pattern of step i+1 on a second stream during step i's attention",
-        "parallelism": f"dp{world} over batch*head ({args.scaling} scaling)",
+        "parallelism": f"dp{world} over batch*head ({args.scaling} scaling)"
+                       + (f", pattern by {args.pattern_exchange}" if world > 1 else ""),
         "l2": "rotating input sets, >= 2x L2 of other data between two uses of a set",
     }
 
@@ -347,6 +348,9 @@ def main():
     ap.add_argument("--no-pipeline", action="store_true",
                     help="run each step's pattern on the attention stream (default: the next step's pattern "
                          "runs on a second stream, concurrent with this step's attention)")
+    ap.add_argument("--pattern-exchange", default="allreduce", choices=["allreduce", "broadcast"],
+                    help="N ranks: sum per-rank partial pools (each rank pools L/N score rows) or broadcast "
+                         "rank 0's pattern")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="cpu_baseline leg: seconds of oracle work")
     ap.add_argument("--cpu-budget-total", type=float, default=120.0, help="--impl reference: seconds for the run")
@@ -368,7 +372,7 @@ def main():
 
     from paper_2309_12578_b200 import spion
     from paper_2309_12578_b200 import _native as N
-    from paper_2309_12578_b200.dist import broadcast_pattern
+    from paper_2309_12578_b200.dist import allreduce_pool, broadcast_pattern, pattern_rows
 
     dist, rank, world, local = dist_setup()
     dev = torch.device(f"cuda:{local}")
@@ -399,27 +403,51 @@ def main():
     bps = [spion.empty_pattern(L, B, dev) for _ in range(NSETS)]
     stream = torch.cuda.Stream(dev)
 
+    # the per-layer pattern with N ranks: each rank pools its slab of score rows, ONE all-reduce sums
+    # the pools, every rank finalises (default); or rank 0 generates it and broadcasts it
+    exchange = None if world == 1 else args.pattern_exchange
+    p0, p1 = pattern_rows(L, B, rank, world)
+
     def make_phases(i):
         A, q, k, v, do = sets[i]
         o, bp = outs[i], bps[i]
-        pat = (lambda: spion.pattern(A, B, filter=FILTER, alpha=args.alpha, out=bp)) if (rank == 0 or world == 1) \
-            else None
+        fin = None
+        if exchange == "allreduce":
+            pat = lambda: spion.pattern_pool(A[p0:p1], L, B, filter=FILTER, row_begin=p0, out=bp)
+            fin = lambda: spion.pattern_finalize(bp, alpha=args.alpha)
+        elif exchange == "broadcast" and rank != 0:
+            pat = None
+        else:
+            pat = lambda: spion.pattern(A, B, filter=FILTER, alpha=args.alpha, out=bp)
         fwd = lambda: spion.attn_fwd(q, k, v, bp, args.mode, scale, out=o["o"], lse=o["lse"], workspace=o["ws"])
         bwd = lambda: spion.attn_bwd(q, k, v, o["o"], do, o["lse"], bp, args.mode, scale, workspace=o["ws"],
                                      dq=o["dq"], dk=o["dk"], dv=o["dv"])
-        return [pat, fwd, bwd]
+        return [pat, fwd, bwd, fin]
+
+    def exchange_pattern(j):
+        """The one collective of the step (NCCL over NVLink; outside the CUDA graphs)."""
+        if exchange == "allreduce":
+            allreduce_pool(spion.pool_region(bps[j]))
+        elif exchange == "broadcast":
+            broadcast_pattern(bps[j].flat, src=0)
 
     with torch.cuda.stream(stream):
         # eager pass first: allocates every pattern workspace, fills the descriptor caches, and
         # counts this library's kernel launches per step
         l0 = spion.launch_count()
         for i in range(NSETS):
-            for fn in make_phases(i):
+            pat, fwd, bwd, fin = make_phases(i)
+            if pat is not None:
+                pat()
+            exchange_pattern(i)
+            for fn in (fin, fwd, bwd):
                 if fn is not None:
                     fn()
-        if world > 1:
-            for bp in bps:
-                broadcast_pattern(bp.flat, src=0)
+        if exchange == "allreduce":  # every rank holds exactly the one-device pattern (checked once)
+            for i in range(NSETS):
+                ref = spion.pattern(sets[i][0], B, filter=FILTER, alpha=args.alpha)
+                if not torch.equal(ref.flat, bps[i].flat):
+                    raise RuntimeError(f"rank {rank}: all-reduced pattern differs from the one-device pattern")
         launches_per_step = (spion.launch_count() - l0) / NSETS
         torch.cuda.synchronize()
         phases = [Phases(make_phases(i), not args.no_graphs, stream) for i in range(NSETS)]
@@ -440,8 +468,8 @@ def main():
                 if ev is not None:
                     ev[0].record(pstream)
                 phases[j].run(0)
-                if world > 1:
-                    broadcast_pattern(bps[j].flat, src=0)  # the per-layer pattern: one NCCL collective
+                exchange_pattern(j)  # the per-layer pattern: one NCCL collective
+                phases[j].run(3)
                 if ev is not None:
                     ev[1].record(pstream)
                 pat_done[j].record(pstream)
@@ -453,8 +481,8 @@ def main():
                 if ev is not None:
                     ev[0].record(stream)
                 ph.run(0)
-                if world > 1:
-                    broadcast_pattern(bps[j].flat, src=0)  # the per-layer pattern: one NCCL collective
+                exchange_pattern(j)  # the per-layer pattern: one NCCL collective
+                ph.run(3)
                 if ev is not None:
                     ev[1].record(stream)
             else:

@@ -146,6 +146,37 @@ SPION_API spion_status spion_pattern_variant(const float *scores_dev, int32_t L,
                            double threshold, spion_threshold_kind kind, uint32_t variant, void *ws_dev,
                            size_t ws_bytes, spion_bsr *out, int32_t *nnzb_host, void *stream);
 
+/* Pattern generation split for a multi-device job.  Eq. 3 and
+ * Eq. 4 are sums over the source rows of A^s, so the pool of the
+ * whole matrix is the SUM of the pools of any partition of its rows: each
+ * device pools its own rows, the callers sum the pool regions of their
+ * workspaces (e.g. one NCCL all-reduce, 64-bit integer sum: exact and
+ * order-independent), and every device finalises the identical pattern.
+ *
+ * spion_pattern_pool_region: the part of a pattern workspace the callers sum,
+ *   as *count_i64 int64 elements starting *offset_bytes into ws (the pool sums
+ *   and the bad-score count); returns 0 (count 0) for an invalid shape.
+ * spion_pattern_pool: zero-fills the workspace's pool region and adds the
+ *   contributions of source rows [row_begin, row_end) (a2-a4).
+ *   scores_rows_dev: those rows only, [row_end - row_begin][L] fp32 row-major
+ *   (row 0 = source row row_begin), values in [0,1], 16-byte aligned.
+ *   row_begin, row_end: multiples of block, 0 <= row_begin <= row_end <= L
+ *   (an empty range gives a zero pool).  Other parameters as spion_pattern.
+ *   Asynchronous; scores outside [0,1] are counted in the pool region and
+ *   reported by spion_pattern_finalize.
+ * spion_pattern_finalize: threshold, flood fill, diagonal, CSR/CSC and plan
+ *   (a5-a7) from the (summed) pool in ws_dev; threshold, kind, variant, out and
+ *   nnzb_host as spion_pattern_variant (SPION_ERR_DATA if any device saw a bad
+ *   score).  spion_pattern_pool over [0, L) followed by spion_pattern_finalize
+ *   is exactly spion_pattern_variant. */
+SPION_API size_t spion_pattern_pool_region(int32_t L, int32_t block, size_t *offset_bytes);
+SPION_API spion_status spion_pattern_pool(const float *scores_rows_dev, int32_t L, int32_t block, int32_t filter,
+                                          int32_t row_begin, int32_t row_end, void *ws_dev, size_t ws_bytes,
+                                          void *stream);
+SPION_API spion_status spion_pattern_finalize(int32_t L, int32_t block, double threshold, spion_threshold_kind kind,
+                                              uint32_t variant, void *ws_dev, size_t ws_bytes, spion_bsr *out,
+                                              int32_t *nnzb_host, void *stream);
+
 /* Synchronises `stream` and reads the device flag word of a pattern
  * workspace: *flags_host = 0 if every score was finite and in [0,1]. */
 SPION_API spion_status spion_pattern_check(const void *ws_dev, int32_t *flags_host, void *stream);

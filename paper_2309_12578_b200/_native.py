@@ -85,6 +85,13 @@ EXPORTS = {
                                                                 ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                                 ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t,
                                                                 ctypes.c_void_p, ctypes.c_void_p]),
+    "spion_pattern_pool_region": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
+    "spion_pattern_pool": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
+                                          ctypes.c_void_p]),
+    "spion_pattern_finalize": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int,
+                                              ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(BSR),
+                                              ctypes.c_void_p, ctypes.c_void_p]),
     "spion_launch_count": (ctypes.c_int64, []),
     "spion_tc_launch_count": (ctypes.c_int64, []),
     "spion_transition": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,

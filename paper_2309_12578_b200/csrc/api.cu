@@ -165,6 +165,56 @@ spion_status spion_pattern_variant(const float *scores_dev, int32_t L, int32_t b
     return SPION_OK;
 }
 
+size_t spion_pattern_pool_region(int32_t L, int32_t block, size_t *offset_bytes) {
+    if (offset_bytes) *offset_bytes = 0;
+    if (L <= 0 || block <= 0 || L % block) return 0;
+    const size_t n = (size_t)(L / block);
+    if (offset_bytes) *offset_bytes = 8;  // the bad-score count, padding, then the pool (at 256)
+    return (256 - 8) / 8 + n * n;
+}
+
+spion_status spion_pattern_pool(const float *scores_rows_dev, int32_t L, int32_t block, int32_t filter,
+                                int32_t row_begin, int32_t row_end, void *ws_dev, size_t ws_bytes, void *stream) {
+    PatternParams pp;
+    spion_status st = pattern_params(L, block, filter, 50.0, SPION_TH_QUANTILE_LINEAR, 0, &pp);
+    if (st) return st;
+    if (row_begin < 0 || row_end < row_begin || row_end > L || row_begin % block || row_end % block)
+        return SPION_ERR_SHAPE;
+    if (!ws_dev || (!scores_rows_dev && row_end > row_begin)) return SPION_ERR_PARAM;
+    if (!aligned16(ws_dev) || (scores_rows_dev && !aligned16(scores_rows_dev))) return SPION_ERR_ALIGN;
+    if (ws_bytes < pattern_ws_bytes(L, block)) return SPION_ERR_WORKSPACE;
+    return launch_pattern_pool(scores_rows_dev, L, block, filter, row_begin, row_end, ws_dev,
+                               static_cast<cudaStream_t>(stream));
+}
+
+spion_status spion_pattern_finalize(int32_t L, int32_t block, double threshold, spion_threshold_kind kind,
+                                    uint32_t variant, void *ws_dev, size_t ws_bytes, spion_bsr *out,
+                                    int32_t *nnzb_host, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PatternParams pp;
+    spion_status st = pattern_params(L, block, 1, threshold, kind, variant, &pp);
+    if (st) return st;
+    if (!ws_dev) return SPION_ERR_PARAM;
+    if (!aligned16(ws_dev)) return SPION_ERR_ALIGN;
+    if (ws_bytes < pattern_ws_bytes(L, block)) return SPION_ERR_WORKSPACE;
+    st = check_bsr_out(out, L, block);
+    if (st) return st;
+    out->L = L;
+    out->block = block;
+    out->nblk = L / block;
+    st = launch_pattern_finalize(L, block, (int)kind, pp.lo, pp.frac_pos, (int)variant, pp.T_abs, ws_dev, out, s);
+    if (st) return st;
+    if (nnzb_host) {
+        int flags = 0;
+        SPION_CUDA_TRY(cudaMemcpyAsync(nnzb_host, out->nnzb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SPION_CUDA_TRY(cudaMemcpyAsync(&flags, ws_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SPION_CUDA_TRY(cudaStreamSynchronize(s));
+        if (flags & FLAG_BAD_SCORE) return SPION_ERR_DATA;
+        if (flags & FLAG_CAPACITY) return SPION_ERR_WORKSPACE;
+    }
+    return SPION_OK;
+}
+
 spion_status spion_pattern_check(const void *ws_dev, int32_t *flags_host, void *stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!ws_dev || !flags_host) return SPION_ERR_PARAM;

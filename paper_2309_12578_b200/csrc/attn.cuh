@@ -62,6 +62,10 @@ spion_status launch_dropout_residual(const void *y, const void *e, void *out, in
 
 // pattern kernels; pattern.cu
 size_t pattern_ws_bytes(int L, int block);
+spion_status launch_pattern_pool(const float *scores_rows, int L, int B, int F, int row_begin, int row_end, void *ws,
+                                 cudaStream_t s);
+spion_status launch_pattern_finalize(int L, int B, int kind, long long lo, int frac_pos, int variant, long long T_abs,
+                                     void *ws, spion_bsr *out, cudaStream_t s);
 spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos, int variant,
                             long long T_abs, void *ws, spion_bsr *out, cudaStream_t s);
 spion_status launch_bsr_from_mask(const uint8_t *mask, int L, int B, spion_bsr *out, int *flags, cudaStream_t s);

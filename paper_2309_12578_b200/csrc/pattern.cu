@@ -40,12 +40,15 @@ static constexpr int K1_MAXP = 2;  // (target row, column) pairs per lane
 
 struct K1Geom {
     int L, B, h, A, nI, JC, n_cc, RP;  // RP: source rows per CTA (grid.z splits the B rows)
+    int Ioff, nrows;                   // the launch covers source block rows [Ioff, Ioff + nrows)
 };
 
 // Window of one CTA: positions [g4, g4 + 128*K4) of a source row (float4-aligned, g4 <= c0);
 // lane l owns positions [4*K4*l, 4*K4*(l+1)).
-static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
+static bool k1_geom(int L, int B, int F, int K4, K1Geom &g, int Ioff = 0, int nrows = -1) {
     g.L = L;
+    g.Ioff = Ioff;
+    g.nrows = nrows < 0 ? L / B : nrows;
     g.B = B;
     g.h = (F - 1) / 2;
     g.A = (g.h + B - 1) / B;
@@ -69,7 +72,7 @@ static bool k1_geom(int L, int B, int F, int K4, K1Geom &g) {
     int rs = 1;
     double best = -1.0;
     for (int r = 1; r == 1 || B / r >= SPION_K1_MIN_ROWS * K1_WARPS; r *= 2) {
-        const double w = (double)g.n_cc * n * r / slots, eff = w / ceil(w);
+        const double w = (double)g.n_cc * g.nrows * r / slots, eff = w / ceil(w);
         if (eff > best + 1e-9) { best = eff; rs = r; }
     }
     g.RP = (B + rs - 1) / rs;
@@ -96,13 +99,15 @@ struct K1Cfg {
 template <int K4>
 __global__ void __launch_bounds__(K1_WARPS * 32, K4 == 4 ? SPION_K1_PER_SM : 1)
 pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *__restrict__ pool,
-                    int *__restrict__ flags) {
+                    unsigned long long *__restrict__ bad_count) {
     using C = K1Cfg<K4>;
     constexpr int CH = C::CH;
     extern __shared__ __align__(16) unsigned char k1_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = g.L, B = g.B, h = g.h, n = L / B;
-    const int cc = blockIdx.x, I0 = blockIdx.y;
+    // A: the rows of the launch's source block rows (row 0 = source row Ioff * B); I0: the block row
+    // in the pool's index space
+    const int cc = blockIdx.x, I0 = blockIdx.y + g.Ioff;
     const int J0 = cc * g.JC;
     const int ncols = min(g.JC, n - J0);
     const int W = ncols * B + 2 * h;  // window-relative columns k in [0, W], column = c0 + k
@@ -141,7 +146,7 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
     __syncthreads();
 
     auto load_row = [&](int u, float4 (&dst)[K4]) {
-        const float *arow = A + (size_t)(I0 * B + u) * L + colbase;
+        const float *arow = A + (size_t)(blockIdx.y * B + u) * L + colbase;
 #pragma unroll
         for (int i = 0; i < K4; ++i)
             dst[i] = ((vmask >> i) & 1u) ? __ldg(reinterpret_cast<const float4 *>(arow + 128 * i))
@@ -251,7 +256,8 @@ pattern_pool_kernel(const float *__restrict__ A, K1Geom g, unsigned long long *_
         const int p = lane + 32 * t;
         if (p < npairs && acc[t]) atomicAdd(&s_acc[p], acc[t]);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, FLAG_BAD_SCORE);
+    // warps that saw a score outside [0, 1] (a sum, so partial pools of several devices add up)
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicAdd(bad_count, 1ull);
     __syncthreads();
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
         const int a = p / ncols - g.A, jj = p % ncols;
@@ -267,13 +273,12 @@ static size_t k1_smem_bytes(const K1Geom &g) {
 }
 
 template <int K4>
-static spion_status k1_launch(const float *scores, const K1Geom &g, unsigned long long *pool, int *flags,
-                              cudaStream_t s) {
+static spion_status k1_launch(const float *scores, const K1Geom &g, unsigned long long *pool,
+                              unsigned long long *bad, cudaStream_t s) {
     static PerDevice attr;
     SPION_CUDA_TRY(smem_attr_once(attr, pattern_pool_kernel<K4>));
-    const int n = g.L / g.B;
     const int rs = (g.B + g.RP - 1) / g.RP;
-    pattern_pool_kernel<K4><<<dim3(g.n_cc, n, rs), K1_WARPS * 32, k1_smem_bytes<K4>(g), s>>>(scores, g, pool, flags);
+    pattern_pool_kernel<K4><<<dim3(g.n_cc, g.nrows, rs), K1_WARPS * 32, k1_smem_bytes<K4>(g), s>>>(scores, g, pool, bad);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
 }
@@ -391,6 +396,7 @@ struct K2Args {
     long long T_abs;        // ABSOLUTE: gt <=> x > T_abs
     int variant;            // spion_pattern_flags
     int *flags;
+    const unsigned long long *bad;  // K1's count of warps that saw a score outside [0, 1] (nullable)
     int *brow_ptr, *bcol_idx, *bcol_ptr, *brow_idx, *nnzb;
     uint8_t *mask;
     int nnzb_cap;
@@ -603,6 +609,7 @@ static __host__ __device__ constexpr int k2_bits_words() { return 4 * K2_MAXN; }
 __global__ void __launch_bounds__(K2_THREADS) pattern_finalize_kernel(K2Args a) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
     const int n = a.n, N = n * n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0 && a.bad && *a.bad && a.flags) atomicOr(a.flags, FLAG_BAD_SCORE);
     long long *s_pool = reinterpret_cast<long long *>(k2_smem);
     unsigned *gtw = reinterpret_cast<unsigned *>(s_pool + ((N + 1) & ~1));  // [n][4] row bitboards: > t
     unsigned *dnw = gtw + k2_bits_words();                      // edge (r,c) -> (r+1,c)
@@ -815,26 +822,40 @@ static size_t k2_smem_bytes(int n, bool with_pool) {
     return b;
 }
 
-spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos, int variant,
-                            long long T_abs, void *ws, spion_bsr *out, cudaStream_t s) {
+// pattern workspace: [0, 4) flags (K2; reported by the ABI), [8, 16) K1's bad-score count (u64),
+// [256, 256 + 8 n^2) the pool sums (i64).  [8, 256 + 8 n^2) is the part a multi-device caller sums.
+static constexpr size_t PWS_BAD = 8, PWS_POOL = 256;
+
+spion_status launch_pattern_pool(const float *scores_rows, int L, int B, int F, int row_begin, int row_end, void *ws,
+                                 cudaStream_t s) {
     const int n = L / B;
     if (n > K2_MAXN) return SPION_ERR_UNSUPPORTED;
-    int *flags = reinterpret_cast<int *>(ws);
-    unsigned long long *pool = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + 256);
-    SPION_CUDA_TRY(cudaMemsetAsync(ws, 0, 256 + (size_t)n * n * 8, s));
+    char *w = static_cast<char *>(ws);
+    unsigned long long *bad = reinterpret_cast<unsigned long long *>(w + PWS_BAD);
+    unsigned long long *pool = reinterpret_cast<unsigned long long *>(w + PWS_POOL);
+    SPION_CUDA_TRY(cudaMemsetAsync(ws, 0, PWS_POOL + (size_t)n * n * 8, s));
+    const int I0 = row_begin / B, nr = (row_end - row_begin) / B;
+    if (nr == 0) return SPION_OK;
     K1Geom g4, g8, g;
     spion_status st;
-    const bool ok4 = k1_geom(L, B, F, 4, g4), ok8 = k1_geom(L, B, F, 8, g8);
+    const bool ok4 = k1_geom(L, B, F, 4, g4, I0, nr), ok8 = k1_geom(L, B, F, 8, g8, I0, nr);
     // fewest window positions per source row (ties: the 16-position lanes, more CTAs)
-    if (ok4 && (!ok8 || g4.n_cc * 4 <= g8.n_cc * 8)) st = k1_launch<4>(scores, g4, pool, flags, s);
-    else if (ok8) st = k1_launch<8>(scores, g8, pool, flags, s);
-    else if (k1_geom(L, B, F, 17, g)) st = k1_launch<17>(scores, g, pool, flags, s);
+    if (ok4 && (!ok8 || g4.n_cc * 4 <= g8.n_cc * 8)) st = k1_launch<4>(scores_rows, g4, pool, bad, s);
+    else if (ok8) st = k1_launch<8>(scores_rows, g8, pool, bad, s);
+    else if (k1_geom(L, B, F, 17, g, I0, nr)) st = k1_launch<17>(scores_rows, g, pool, bad, s);
     else return SPION_ERR_UNSUPPORTED;  // B + F > ~2170 columns per window
-    if (st != SPION_OK) return st;
+    return st;
+}
 
+spion_status launch_pattern_finalize(int L, int B, int kind, long long lo, int frac_pos, int variant, long long T_abs,
+                                     void *ws, spion_bsr *out, cudaStream_t s) {
+    const int n = L / B;
+    if (n > K2_MAXN) return SPION_ERR_UNSUPPORTED;
+    char *w = static_cast<char *>(ws);
     K2Args a;
     memset(&a, 0, sizeof(a));
-    a.pool = reinterpret_cast<const long long *>(pool);
+    a.pool = reinterpret_cast<const long long *>(w + PWS_POOL);
+    a.bad = reinterpret_cast<const unsigned long long *>(w + PWS_BAD);
     a.n = n;
     a.block = B;
     a.kind = kind;
@@ -842,7 +863,7 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     a.frac_pos = frac_pos;
     a.T_abs = T_abs;
     a.variant = variant;
-    a.flags = flags;
+    a.flags = reinterpret_cast<int *>(ws);
     a.brow_ptr = out->brow_ptr;
     a.bcol_idx = out->bcol_idx;
     a.bcol_ptr = out->bcol_ptr;
@@ -864,6 +885,13 @@ spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, 
     pattern_finalize_kernel<<<1, K2_THREADS, smem2, s>>>(a);
     SPION_LAUNCH_CHECK();
     return SPION_OK;
+}
+
+spion_status launch_pattern(const float *scores, int L, int B, int F, int kind, long long lo, int frac_pos, int variant,
+                            long long T_abs, void *ws, spion_bsr *out, cudaStream_t s) {
+    spion_status st = launch_pattern_pool(scores, L, B, F, 0, L, ws, s);
+    if (st) return st;
+    return launch_pattern_finalize(L, B, kind, lo, frac_pos, variant, T_abs, ws, out, s);
 }
 
 spion_status launch_bsr_from_mask(const uint8_t *mask, int L, int B, spion_bsr *out, int *flags, cudaStream_t s) {

@@ -130,6 +130,61 @@ def pattern(scores: torch.Tensor, block: int, filter: int = 31, alpha: Optional[
     return bp
 
 
+def _pattern_ws(bp: BlockPattern, device) -> int:
+    ws_bytes = N.lib().spion_pattern_workspace_bytes(bp.L, bp.block)
+    if bp.workspace is None or bp.workspace.numel() < ws_bytes:
+        bp.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    return ws_bytes
+
+
+def pattern_pool(scores_rows: torch.Tensor, L: int, block: int, filter: int = 31, row_begin: int = 0,
+                 out: Optional[BlockPattern] = None) -> BlockPattern:
+    """Eq. 3-4 over source rows [row_begin, row_begin + rows) of an L x L score
+    matrix, given as those rows only (``scores_rows``: [rows][L] fp32), into the pool region of
+    ``out.workspace`` (zero-filled first).  Pools of a row partition add up to the whole matrix's
+    pool: sum ``pool_region(bp)`` over the devices (one all-reduce), then ``pattern_finalize``."""
+    _require_cuda(scores_rows)
+    if scores_rows.dtype != torch.float32 or scores_rows.dim() != 2 or scores_rows.shape[1] != L:
+        raise ValueError("scores_rows must be fp32 [rows][L]")
+    scores_rows = scores_rows.contiguous()
+    bp = out if out is not None else empty_pattern(L, block, scores_rows.device)
+    ws_bytes = _pattern_ws(bp, scores_rows.device)
+    rows = scores_rows.shape[0]
+    st = N.lib().spion_pattern_pool(_p(scores_rows) if rows else None, L, block, filter, row_begin, row_begin + rows,
+                                    _p(bp.workspace), ws_bytes, _stream(scores_rows.device))
+    N.check(st, "spion_pattern_pool")
+    return bp
+
+
+def pool_region(bp: BlockPattern) -> torch.Tensor:
+    """int64 view of the part of ``bp.workspace`` that devices sum (pool sums + bad-score count)."""
+    off = ctypes.c_size_t(0)
+    cnt = N.lib().spion_pattern_pool_region(bp.L, bp.block, ctypes.byref(off))
+    return bp.workspace[off.value: off.value + 8 * cnt].view(torch.int64)
+
+
+def pattern_finalize(bp: BlockPattern, alpha: Optional[float] = None, t: Optional[float] = None,
+                     kind: str = "linear", variant: str = "", sync: bool = False) -> BlockPattern:
+    """Threshold, flood fill, diagonal, CSR/CSC and plan (Alg. 3 l.4-end) from the pool in
+    ``bp.workspace`` (after ``pattern_pool`` and, on several devices, the sum of ``pool_region``)."""
+    if t is not None:
+        kind, theta = "absolute", float(t)
+    else:
+        if alpha is None:
+            raise ValueError("give alpha or t")
+        theta = float(alpha)
+    if bp.workspace is None:
+        raise ValueError("pattern_finalize needs the workspace pattern_pool filled")
+    s = bp.c_struct()
+    nnz = ctypes.c_int32(0)
+    bits = sum(N.PATTERN_VARIANTS[v] for v in variant.split("+")) if variant else 0
+    st = N.lib().spion_pattern_finalize(bp.L, bp.block, theta, N.THRESH[kind], bits, _p(bp.workspace),
+                                        bp.workspace.numel(), ctypes.byref(s), ctypes.byref(nnz) if sync else None,
+                                        _stream(bp.workspace.device))
+    N.check(st, "spion_pattern_finalize")
+    return bp
+
+
 def bsr_from_mask(mask: torch.Tensor, L: int, block: int, out: Optional[BlockPattern] = None) -> BlockPattern:
     """Block pattern from a caller-supplied [nblk][nblk] {0,1} uint8 mask (device)."""
     _require_cuda(mask)

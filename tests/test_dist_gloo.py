@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2309_12578_b200.dist import broadcast_pattern, shard
+from paper_2309_12578_b200.dist import allreduce_pool, broadcast_pattern, pattern_rows, shard
 
 
 def test_shard_partitions_exactly():
@@ -171,3 +171,57 @@ def test_gloo_world2_broadcast_and_sharding():
     for rank, ok_bcast, ok_shard, tmax in res:
         assert ok_bcast and ok_shard
         assert tmax == 2.0
+
+
+def _worker_pool(rank, world, port, out_q):
+    """The bench's default multi-GPU pattern exchange on CPU: each rank pools its own slab of score
+    rows (the oracle's Eq. 3-4 on the matrix that keeps only those rows, as spion_pattern_pool
+    computes on the rank's GPU), ONE all-reduce sums the int64 pools, and every rank thresholds and
+    flood-fills the sum: every rank holds exactly the 1-rank pattern."""
+    import numpy as np
+
+    import oracle
+    import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ok = True
+        for L, B, F, alpha in ((64, 8, 31, 75.0), (96, 4, 63, 60.0), (256, 32, 31, 90.0)):
+            A = synth.syn_scores(L, B, heads=2, seed=L + F).numpy()
+            r0, r1 = pattern_rows(L, B, rank, world)
+            As = np.zeros_like(A)
+            As[r0:r1] = A[r0:r1]
+            part = oracle.pool_sum(oracle.diag_conv(oracle.quantize(As), F), B)
+            region = torch.from_numpy(part.reshape(-1).copy())
+            allreduce_pool(region)
+            pool = region.numpy().reshape(part.shape)
+            gt, _ = oracle.threshold_gt(pool, B, alpha)
+            fl = oracle.flood_fill(pool, gt)
+            fl_ref, _, _ = oracle.pattern(A, B, F, alpha)
+            ok &= bool((fl == fl_ref).all())
+        out_q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pattern_rows_partition():
+    for L, B in ((64, 8), (1024, 32), (4096, 64), (96, 4)):
+        for world in (1, 2, 3, 4, 8):
+            r = [pattern_rows(L, B, k, world) for k in range(world)]
+            assert r[0][0] == 0 and r[-1][1] == L and all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+            assert all(a % B == 0 and b % B == 0 for a, b in r)
+
+
+def test_gloo_world2_pool_allreduce_pattern():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_pool, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok for _, ok in res), res

@@ -140,3 +140,77 @@ def test_pattern_variants_ties(seed, variant):
         bp = spion.pattern(torch.from_numpy(A).to(DEV), B, filter=7, alpha=alpha, sync=True, variant=variant)
         fl_ref, _, _ = oracle.pattern(A, B, 7, alpha, variant=variant)
         _check(bp, fl_ref)
+
+
+# ---------------------------------------------------------------- multi-device pattern path
+SPLIT_CASES = [
+    # L, B, F, theta, row cuts (multiples of B; the multi-device bench uses n / world block rows each)
+    (64, 8, 31, 75.0, [32]),
+    (1024, 32, 31, 75.0, [256, 512, 768]),     # LRA Image over 4 devices
+    (2048, 64, 31, 75.0, [1024]),
+    (4096, 64, 31, 55.0, [512 * k for k in range(1, 8)]),  # Text over 8 devices
+    (96, 4, 63, 60.0, [4, 48, 92]),            # h > B: taps reach pool rows of other slabs
+    (1280, 10, 31, 75.0, [0, 640, 1280]),      # empty first and last slab, B not a multiple of 4
+]
+
+
+def _pool_of(bp, n):
+    spion = _spion()
+    return spion.pool_region(bp)[-n * n:].view(n, n)
+
+
+@pytest.mark.parametrize("L,B,F,theta,cuts", SPLIT_CASES)
+def test_pattern_pool_partition_sum_finalize(L, B, F, theta, cuts):
+    """spion_pattern_pool on every slab of a row partition (one workspace each, as one device each),
+    the pool regions summed (what an all-reduce does), spion_pattern_finalize: the same pattern as
+    spion_pattern, bit for bit; each slab's partial pool equals the oracle pool of the matrix that
+    keeps only that slab's rows."""
+    spion = _spion()
+    A = synth.syn_scores(L, B, heads=2, seed=L + B + F)
+    Ad = A.to(DEV)
+    n = L // B
+    edges = [0] + cuts + [L]
+    parts = []
+    for r0, r1 in zip(edges[:-1], edges[1:]):
+        bp = spion.pattern_pool(Ad[r0:r1], L, B, filter=F, row_begin=r0)
+        As = np.zeros_like(A.numpy())
+        As[r0:r1] = A.numpy()[r0:r1]
+        ref = oracle.pool_sum(oracle.diag_conv(oracle.quantize(As), F), B)
+        assert (_pool_of(bp, n).cpu().numpy() == ref).all(), (r0, r1)
+        parts.append(bp)
+    total = parts[0]
+    region = spion.pool_region(total)
+    for bp in parts[1:]:
+        region += spion.pool_region(bp)
+    spion.pattern_finalize(total, alpha=theta, sync=True)
+    whole = spion.pattern(Ad, B, filter=F, alpha=theta, sync=True)
+    fl_ref, _, _ = oracle.pattern(A.numpy(), B, F, theta)
+    _check(total, fl_ref)
+    assert torch.equal(total.flat, whole.flat)  # CSR, CSC, mask and the attention plan
+
+
+def test_pattern_pool_bad_score_in_one_slab():
+    spion = _spion()
+    from paper_2309_12578_b200 import _native as N
+    L, B = 256, 16
+    A = synth.syn_scores(L, B, heads=1, seed=5)
+    A[200, 3] = 1.5  # outside [0, 1], in the second slab
+    Ad = A.to(DEV)
+    a = spion.pattern_pool(Ad[:128], L, B, row_begin=0)
+    b = spion.pattern_pool(Ad[128:], L, B, row_begin=128)
+    spion.pool_region(a).add_(spion.pool_region(b))
+    with pytest.raises(N.SpionError) as e:
+        spion.pattern_finalize(a, alpha=90.0, sync=True)
+    assert e.value.status == 3  # SPION_ERR_DATA
+
+
+def test_pattern_pool_rejects_bad_ranges():
+    spion = _spion()
+    from paper_2309_12578_b200 import _native as N
+    L, B = 256, 16
+    A = synth.syn_scores(L, B, heads=1, seed=6).to(DEV)
+    with pytest.raises(N.SpionError) as e:
+        spion.pattern_pool(A[8:40], L, B, row_begin=8)  # not at a block boundary
+    assert e.value.status == 1  # SPION_ERR_SHAPE
+    with pytest.raises(N.SpionError):
+        spion.pattern_pool(A[:64], L, B, row_begin=224)  # past L

@@ -416,3 +416,27 @@ def test_variants_worked_example(golden_dir):
     for case in g["cases"]:
         for v, want in case["fl"].items():
             assert (_var(case["pool"], case["t"], v) == np.array(want, np.uint8)).all(), v
+
+
+@pytest.mark.parametrize("L,B,F,cuts", [(64, 8, 31, [24]), (96, 4, 63, [32, 36, 80]), (128, 16, 3, [0, 64, 128]),
+                                        (256, 32, 31, [96, 160])])
+def test_pool_is_sum_over_row_partition(L, B, F, cuts):
+    """Eq. 3-4 are sums over the source rows of A^s: the pool of the whole matrix is the
+    sum of the pools of the matrices that keep one slab of rows each (zeros elsewhere) — including
+    slabs whose diagonal-filter taps (h > B for F=63, B=4) reach pool rows of a neighbouring slab.
+    This is what the multi-device pattern path (spion_pattern_pool + a sum + spion_pattern_finalize)
+    relies on; checked here against a direct pool of the unsplit matrix."""
+    A = syn_scores(L, B, heads=2, seed=L + F)
+    full = oracle.pool_sum(oracle.diag_conv(oracle.quantize(A.numpy()), F), B)
+    edges = [0] + [c for c in cuts] + [L]
+    acc = np.zeros_like(full)
+    for r0, r1 in zip(edges[:-1], edges[1:]):
+        As = np.zeros_like(A.numpy())
+        As[r0:r1] = A.numpy()[r0:r1]
+        acc += oracle.pool_sum(oracle.diag_conv(oracle.quantize(As), F), B)
+    assert (acc == full).all()
+    # and the pattern from the summed pool is the pattern of the matrix
+    gt, _ = oracle.threshold_gt(acc, B, 75.0)
+    fl = oracle.flood_fill(acc, gt)
+    fl_ref, _, _ = oracle.pattern(A.numpy(), B, F, 75.0)
+    assert (fl == fl_ref).all()
