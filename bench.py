@@ -80,7 +80,8 @@ def config_dict(cfg, args, world):
         "workload": cfg["workload"], "L": cfg["L"], "block": cfg["block"], "heads": cfg["heads"], "d": cfg["d"],
         "batch": cfg["batch"], "towers": cfg["towers"], "bh": bh, "filter": FILTER, "alpha": args.alpha,
         "softmax": args.mode, "step": "pattern(scores)+attn_fwd+attn_bwd",
-        "pipeline": "sequential" if args.no_pipeline else "pattern of step i+1 on a second stream during step i's attention",
+        "pipeline": "sequential" if args.no_pipeline else
+        f"pattern of step i+{args.pipeline_depth} on a second stream during step i's attention",
         "parallelism": f"dp{world} over batch*head ({args.scaling} scaling)"
                        + (f", pattern by {args.pattern_exchange}" if world > 1 else ""),
         "l2": "rotating input sets, >= 2x L2 of other data between two uses of a set",
@@ -351,6 +352,10 @@ def main():
     ap.add_argument("--pattern-exchange", default="allreduce", choices=["allreduce", "broadcast"],
                     help="N ranks: sum per-rank partial pools (each rank pools L/N score rows) or broadcast "
                          "rank 0's pattern")
+    ap.add_argument("--pipeline-depth", type=int, default=None,
+                    help="pipelined steps: step i launches the pattern of step i+D (default 1 on one GPU; 3 with "
+                         "N ranks, where a rank's attention share is shorter than the pattern's latency: "
+                         "K2 + the collective)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="cpu_baseline leg: seconds of oracle work")
     ap.add_argument("--cpu-budget-total", type=float, default=120.0, help="--impl reference: seconds for the run")
@@ -361,6 +366,8 @@ def main():
         args.alpha = cfg["alpha"]
     if args.warmup < 3:
         args.warmup = 3
+    if args.pipeline_depth is None:
+        args.pipeline_depth = 1 if int(os.environ.get("WORLD_SIZE", args.gpus)) <= 1 else 3
     if maybe_self_launch(args):
         return
     if args.impl == "reference":
@@ -390,7 +397,9 @@ def main():
     # of other data is touched (a step never finds its inputs in L2)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     set_bytes = 4 * L * L + 9 * bh * L * d * 2 + 2 * bh * L * 4
-    NSETS = max(2, min(16, math.ceil(2 * l2 / set_bytes) + 1))
+    # input sets in rotation (each with its own pattern buffer): >= 2, and one more than the pattern
+    # look-ahead so pattern i+D never overwrites a buffer an unfinished step still reads
+    NSETS = max(2, 1 + (0 if args.no_pipeline else args.pipeline_depth), min(16, math.ceil(2 * l2 / set_bytes) + 1))
     scores_cpu = [synth.lra_scores(L, B, seed=sd) for sd in SCORE_SEEDS]
     sets, outs = [], []
     for s in range(NSETS):
@@ -497,10 +506,11 @@ def main():
                 ev[4].record(stream)
             if not args.no_pipeline:
                 att_done[j].record(stream)
-                pattern_on_pstream((i + 1) % NSETS, ev[5:] if ev is not None else None)
+                pattern_on_pstream((i + args.pipeline_depth) % NSETS, ev[5:] if ev is not None else None)
 
         if not args.no_pipeline:
-            pattern_on_pstream(0)
+            for j in range(args.pipeline_depth):
+                pattern_on_pstream(j % NSETS)
         for i in range(args.warmup):
             step(i)
         torch.cuda.synchronize()
@@ -518,7 +528,8 @@ def main():
         for i in range(args.warmup, args.warmup + args.steps):
             step(i, evs[i - args.warmup])
         if not args.no_pipeline:
-            stream.wait_event(pat_done[(args.warmup + args.steps) % NSETS])  # the K-th pattern of the region
+            # the K-th pattern launched in the region
+            stream.wait_event(pat_done[(args.warmup + args.steps + args.pipeline_depth - 1) % NSETS])
         end.record(stream)
         torch.cuda.synchronize()
         barrier(dist)
