@@ -82,8 +82,11 @@ def config_dict(cfg, args, world):
         "softmax": args.mode, "step": "pattern(scores)+attn_fwd+attn_bwd",
         "pipeline": "sequential" if args.no_pipeline else
         f"pattern of step i+{args.pipeline_depth} on a second stream during step i's attention",
-        "parallelism": f"dp{world} over batch*head ({args.scaling} scaling)"
-                       + (f", pattern by {args.pattern_exchange}" if world > 1 else ""),
+        "parallelism": (f"emulated: rank 0's share of dp{args.emulate_world} over batch*head ({args.scaling} "
+                        "scaling) on one GPU; the all-reduced pool arrives by a device copy"
+                        if world == 1 and args.emulate_world > 1 else
+                        f"dp{world} over batch*head ({args.scaling} scaling)"
+                        + (f", pattern by {args.pattern_exchange}" if world > 1 else "")),
         "l2": "rotating input sets, >= 2x L2 of other data between two uses of a set",
     }
 
@@ -356,6 +359,10 @@ def main():
                     help="pipelined steps: step i launches the pattern of step i+D (default 1 on one GPU; 3 with "
                          "N ranks, where a rank's attention share is shorter than the pattern's latency: "
                          "K2 + the collective)")
+    ap.add_argument("--emulate-world", type=int, default=1,
+                    help="one GPU: run rank 0's share of an E-rank job (its (batch, head) shard, its slab of the "
+                         "pattern's score rows; the all-reduced pool delivered by a device copy) to project "
+                         "strong scaling without the collective's latency; the line adds emulated_world")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="cpu_baseline leg: seconds of oracle work")
     ap.add_argument("--cpu-budget-total", type=float, default=120.0, help="--impl reference: seconds for the run")
@@ -367,7 +374,7 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.pipeline_depth is None:
-        args.pipeline_depth = 1 if int(os.environ.get("WORLD_SIZE", args.gpus)) <= 1 else 3
+        args.pipeline_depth = 1 if max(int(os.environ.get("WORLD_SIZE", args.gpus)), args.emulate_world) <= 1 else 3
     if maybe_self_launch(args):
         return
     if args.impl == "reference":
@@ -387,9 +394,10 @@ def main():
     hbm_peak, tc_peak, tc_sust, peak_src = load_peaks()
 
     L, B, H, d = cfg["L"], cfg["block"], cfg["heads"], cfg["d"]
-    s0, s1 = rank_slices(cfg, args.scaling, rank, world)
+    emu = args.emulate_world if world == 1 else 1     # --emulate-world E: rank 0's share of E ranks
+    s0, s1 = rank_slices(cfg, args.scaling, rank, max(world, emu))
     bh = s1 - s0                                         # this rank's (batch, head) slices
-    bh_total = cfg["batch"] * cfg["towers"] * H * (world if args.scaling == "weak" else 1)
+    bh_total = cfg["batch"] * cfg["towers"] * H * (max(world, emu) if args.scaling == "weak" else 1)
     tokens_job = bh_total // H * L                       # tokens of the whole job per step
     scale = 1.0 / math.sqrt(d)
 
@@ -414,14 +422,19 @@ def main():
 
     # the per-layer pattern with N ranks: each rank pools its slab of score rows, ONE all-reduce sums
     # the pools, every rank finalises (default); or rank 0 generates it and broadcasts it
-    exchange = None if world == 1 else args.pattern_exchange
-    p0, p1 = pattern_rows(L, B, rank, world)
+    exchange = "emulated" if emu > 1 else (None if world == 1 else args.pattern_exchange)
+    p0, p1 = pattern_rows(L, B, rank, max(world, emu))
+    if exchange == "emulated":
+        # what the all-reduce would deliver: the pool region of the whole matrix (computed once)
+        full_regions = [spion.pool_region(spion.pattern_pool(sets[i][0], L, B, filter=FILTER)).clone()
+                        for i in range(NSETS)]
+        torch.cuda.synchronize()
 
     def make_phases(i):
         A, q, k, v, do = sets[i]
         o, bp = outs[i], bps[i]
         fin = None
-        if exchange == "allreduce":
+        if exchange in ("allreduce", "emulated"):
             pat = lambda: spion.pattern_pool(A[p0:p1], L, B, filter=FILTER, row_begin=p0, out=bp)
             fin = lambda: spion.pattern_finalize(bp, alpha=args.alpha)
         elif exchange == "broadcast" and rank != 0:
@@ -437,6 +450,8 @@ def main():
         """The one collective of the step (NCCL over NVLink; outside the CUDA graphs)."""
         if exchange == "allreduce":
             allreduce_pool(spion.pool_region(bps[j]))
+        elif exchange == "emulated":  # one device: the summed pool arrives as a 32 KB device copy
+            spion.pool_region(bps[j]).copy_(full_regions[j])
         elif exchange == "broadcast":
             broadcast_pattern(bps[j].flat, src=0)
 
@@ -452,7 +467,7 @@ def main():
             for fn in (fin, fwd, bwd):
                 if fn is not None:
                     fn()
-        if exchange == "allreduce":  # every rank holds exactly the one-device pattern (checked once)
+        if exchange in ("allreduce", "emulated"):  # every rank holds exactly the one-device pattern (checked once)
             for i in range(NSETS):
                 ref = spion.pattern(sets[i][0], B, filter=FILTER, alpha=args.alpha)
                 if not torch.equal(ref.flat, bps[i].flat):
@@ -623,14 +638,16 @@ def main():
                         "score_seeds": list(SCORE_SEEDS)},
             "bh_per_rank": bh, "input_sets": NSETS, "cuda_graphs": not args.no_graphs,
             "phases_ms": ph_ms,
-            "useful_tflops": step_flops * world / (ms * 1e-3) / 1e12,
-            "pct_bf16_peak_useful": 100.0 * step_flops * world / (ms * 1e-3) / (tc_peak * 1e12 * world),
+            "useful_tflops": step_flops * max(world, emu) / (ms * 1e-3) / 1e12,
+            "pct_bf16_peak_useful": 100.0 * step_flops / (ms * 1e-3) / (tc_peak * 1e12),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if emu > 1:
+            line["emulated_world"] = emu
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -1,6 +1,6 @@
 """Per-kernel mean device time (torch.profiler / CUPTI activity records) of this library's kernels
 over one config's pattern + fwd + bwd, repeated on rotating inputs: A/B diagnostics only (never a
-bench number).  usage: [SPION_LIB=...] python tools/kernel_times.py [config] [reps]"""
+bench number).  usage: [SPION_LIB=...] python tools/kernel_times.py [config] [reps] [E: bh / E]"""
 import collections, math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -11,6 +11,8 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 L, B, H, batch, towers, alpha = {"image": (1024, 32, 4, 64, 1, 75.0), "listops": (2048, 64, 8, 32, 1, 75.0),
                                  "text": (4096, 64, 8, 16, 1, 55.0), "retrieval": (4096, 64, 8, 16, 2, 55.0)}[cfg]
 bh, d = batch * towers * H, 64
+if len(sys.argv) > 3:  # rank 0's share of an E-rank job: bh / E slices
+    bh //= int(sys.argv[3])
 dev = torch.device("cuda:0")
 sets = []
 for s in range(3):
