@@ -335,6 +335,15 @@ def test_full_size_all_slices(cfg):
              lse_tol=1e-3)
 
 
+def _step_chunks(bh, tensor_bytes):
+    """spion_step_host's (batch, head) chunk count (api.cu step_chunks)."""
+    cmax = 8 if tensor_bytes > (64 << 20) else 16
+    for C in (16, 8, 4, 2):
+        if C <= cmax and bh % C == 0 and bh // C >= 8 and tensor_bytes // C >= (4 << 20):
+            return C
+    return 1
+
+
 @pytest.mark.parametrize("bh,dtype,mode", [(16, "bf16", "paper"), (256, "bf16", "paper"), (512, "bf16", "masked"),
                                            (48, "f32", "paper")])
 def test_step_host_matches_device_calls(bh, dtype, mode):
@@ -354,7 +363,14 @@ def test_step_host_matches_device_calls(bh, dtype, mode):
     bp = spion.pattern(A.to(DEV), B, filter=31, alpha=75.0, sync=True)
     qd, kd, vd, dod = (x.to(DEV) for x in (q, k, v, do))
     o, lse = spion.attn_fwd(qd, kd, vd, bp, mode, scale)
-    dq, dk, dv = spion.attn_bwd(qd, kd, vd, o, dod, lse, bp, mode, scale)
+    # the device reference in spion_step_host's (batch, head) chunks: a launch's size decides whether the
+    # dK/dV pass splits its heavy tiles (the summation order of those tiles' dK, dV)
+    C = _step_chunks(bh, bh * L * d * (2 if dtype == "bf16" else 4))
+    bc = bh // C
+    grads = [spion.attn_bwd(qd[c * bc:(c + 1) * bc], kd[c * bc:(c + 1) * bc], vd[c * bc:(c + 1) * bc],
+                            o[c * bc:(c + 1) * bc], dod[c * bc:(c + 1) * bc], lse[c * bc:(c + 1) * bc], bp, mode, scale)
+             for c in range(C)]
+    dq, dk, dv = (torch.cat([g[i] for g in grads]) for i in range(3))
     torch.cuda.synchronize()
     lib = N.lib()
     hA = A.pin_memory()
@@ -598,3 +614,51 @@ def test_full_size_all_slices_masked(cfg):
     outs = _run(q, k, v, do, bp, "masked", 1 / math.sqrt(d))
     _compare(outs, q, k, v, do, fl, B, "masked", 1 / math.sqrt(d), range(bh), 2e-2, norm_tol=1e-2,
              lse_tol=1e-3)
+
+
+# ---------------------------------------------------------------- small launches (one rank's share)
+@pytest.mark.parametrize("cfg,bh", [("text", 16), ("image", 32), ("listops", 8)])
+def test_small_launch_all_slices(cfg, bh):
+    """One rank's share of a strong-scaled job (few (batch, head) per launch, so the heavy tiles — a
+    vertical stripe's ~n entries — are a large part of each CTA's work): every slice against the oracle."""
+    spion = _spion()
+    c = FULL[cfg]
+    L, B, d = c["L"], c["B"], 64
+    A = synth.lra_scores(L, B, seed=1)
+    bp = spion.pattern(A.to(DEV), B, filter=31, alpha=c["alpha"], sync=True)
+    fl, _, _ = oracle.pattern(A.numpy(), B, 31, c["alpha"])
+    q, k, v, do = synth.qkvdo(bh, L, d, seed=77, dtype=torch.bfloat16)
+    outs = _run(q, k, v, do, bp, "paper", 1 / math.sqrt(d))
+    _compare(outs, q, k, v, do, fl, B, "paper", 1 / math.sqrt(d), range(bh), 2e-2, norm_tol=1e-2, lse_tol=1e-3)
+
+
+def test_small_launch_matches_large_launch():
+    """The same (batch, head) slices in a launch of 16 and inside one of 64: the persistent kernels'
+    results do not depend on which CTA takes an item or on the launch's size — bit for bit."""
+    spion = _spion()
+    L, B, d = 4096, 64, 64
+    A = synth.lra_scores(L, B, seed=1001)
+    bp = spion.pattern(A.to(DEV), B, filter=31, alpha=55.0, sync=True)
+    q, k, v, do = (x.to(DEV) for x in synth.qkvdo(64, L, d, seed=31, dtype=torch.bfloat16))
+    o, lse = spion.attn_fwd(q, k, v, bp)
+    big = spion.attn_bwd(q, k, v, o, do, lse, bp)
+    o16, lse16 = spion.attn_fwd(q[:16], k[:16], v[:16], bp)
+    small = spion.attn_bwd(q[:16], k[:16], v[:16], o16, do[:16], lse16, bp)
+    assert torch.equal(o16, o[:16]) and torch.equal(lse16, lse[:16])
+    for a, b in zip(small, big):
+        assert torch.equal(a, b[:16])
+
+
+@pytest.mark.parametrize("mode", ["paper", "masked"])
+def test_single_column_mask(mode):
+    """A caller mask whose only blocks are three in one block column (no diagonal): one heavy column
+    tile, every other tile and most rows empty."""
+    spion = _spion()
+    L, B, d, bh = 1024, 64, 64, 4
+    n = L // B
+    fl = np.zeros((n, n), dtype=np.uint8)
+    fl[[0, 5, 9], 3] = 1
+    bp = spion.bsr_from_mask(torch.from_numpy(fl).to(DEV), L, B)
+    q, k, v, do = synth.qkvdo(bh, L, d, seed=13, dtype=torch.bfloat16)
+    outs = _run(q, k, v, do, bp, mode, 1 / math.sqrt(d))
+    _compare(outs, q, k, v, do, fl, B, mode, 1 / math.sqrt(d), range(bh), 2e-2, norm_tol=1e-2)

@@ -12,6 +12,7 @@ import synth
 from paper_2309_12578_b200 import spion, _native as N
 cfg = sys.argv[1] if len(sys.argv) > 1 else "text"
 L, B, bh = {"image": (1024, 32, 256), "text": (4096, 64, 128), "listops": (2048, 64, 256)}[cfg]
+bh = int(os.environ.get("BH", bh))
 d = 64
 dev = torch.device("cuda:0")
 A = synth.lra_scores(L, B, seed=1, device=dev)
@@ -50,7 +51,8 @@ for role in range(R):
         if len(vv) > 10:
             print("   %-20s -> %-20s n=%4d median %6d" % (names.get(e0, e0), names.get(e1, e1), len(vv), sorted(vv)[len(vv) // 2]))
 lo = int(sys.argv[2]) if len(sys.argv) > 2 else 300
-for c, e, r in evs[lo:lo + 80]:
+WIN = int(os.environ.get("WIN", "80"))
+for c, e, r in evs[lo:lo + WIN]:
     print(f"{c - c0:9d} r{r} {names.get(e, e)}")
 # gaps in the dV/dK warp's issue stream (role 4, event 15 = a block's dV/dK MMAs issued)
 iss = [c for c, e, r in evs if r == 4 and e == 15]
