@@ -153,3 +153,32 @@ def test_status_strings():
     lib = N.lib()
     for k in range(8):
         assert lib.spion_status_str(k)
+
+
+def test_pattern_pool_region_and_split_validation():
+    """The multi-device pattern split (spion_pattern_pool / spion_pattern_finalize): the summable
+    region of a pattern workspace (the int64 pool sums at byte 256 and the bad-score count at byte 8,
+    contiguous) and the host-side rejections, all before any device work (bogus pointers)."""
+    lib = N.lib()
+    off = ctypes.c_size_t(7)
+    for L, B in ((64, 8), (1024, 32), (4096, 64)):
+        n = L // B
+        cnt = lib.spion_pattern_pool_region(L, B, ctypes.byref(off))
+        assert off.value == 8 and cnt == (256 - 8) // 8 + n * n
+        assert off.value + 8 * cnt == lib.spion_pattern_workspace_bytes(L, B) - ((-(n * n * 8)) % 256)
+    assert lib.spion_pattern_pool_region(100, 32, ctypes.byref(off)) == 0 and off.value == 0
+    P = ctypes.c_void_p(1 << 20)  # 16-byte aligned bogus device pointer: never dereferenced
+    ws = lib.spion_pattern_workspace_bytes(256, 16)
+    # row range not at block boundaries / outside [0, L]
+    assert lib.spion_pattern_pool(P, 256, 16, 31, 8, 40, P, ws, None) == 1
+    assert lib.spion_pattern_pool(P, 256, 16, 31, 224, 288, P, ws, None) == 1
+    assert lib.spion_pattern_pool(P, 256, 16, 31, 64, 32, P, ws, None) == 1
+    # even filter, null workspace, misaligned scores, small workspace
+    assert lib.spion_pattern_pool(P, 256, 16, 30, 0, 64, P, ws, None) == 2
+    assert lib.spion_pattern_pool(P, 256, 16, 31, 0, 64, None, ws, None) == 2
+    assert lib.spion_pattern_pool(ctypes.c_void_p((1 << 20) + 4), 256, 16, 31, 0, 64, P, ws, None) == 4
+    assert lib.spion_pattern_pool(P, 256, 16, 31, 0, 64, P, ws - 1, None) == 5
+    # finalize: alpha out of range, unknown variant bits, null output pattern
+    assert lib.spion_pattern_finalize(256, 16, 100.0, N.THRESH["linear"], 0, P, ws, None, None, None) == 2
+    assert lib.spion_pattern_finalize(256, 16, 50.0, N.THRESH["linear"], 8, P, ws, None, None, None) == 2
+    assert lib.spion_pattern_finalize(256, 16, 50.0, N.THRESH["linear"], 0, P, ws, None, None, None) == 2
